@@ -1,0 +1,216 @@
+"""Generate tests/golden/*.npz by running the REFERENCE package itself.
+
+Run in the build container only (it imports /root/reference/pkg/src, which
+does not exist on the GPU box):
+
+    python oracle/gen_golden.py
+
+Every vector here is produced by ``nucleuskv`` (the reference), never by
+this repo's oracle, so ``tests/test_oracle_golden.py`` pins the oracle to
+the reference and the GPU tests pin the CUDA path to the same vectors.
+Inputs are seeded; bf16 cases hold bf16-representable float32 values
+(the oracle/GPU see exactly these numbers).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even float32 -> bfloat16, returned as float32."""
+    a = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    rounded = (a + 0x7FFF + ((a >> 16) & 1)) & 0xFFFF0000
+    return rounded.astype(np.uint32).view(np.float32)
+
+
+def main() -> None:
+    sys.path.insert(0, REF)
+    import nucleuskv as nk
+    from nucleuskv.quantcache import _unpack_matrix
+
+    os.makedirs(OUT, exist_ok=True)
+    rng = np.random.default_rng(20250204)
+
+    # ---------------------------------------------------------- quantization
+    quant = {}
+    cases = {
+        "gauss_f32": rng.standard_normal((203, 128)).astype(np.float32),
+        "gauss_bf16": bf16_round(rng.standard_normal((203, 128)) * 1.7),
+        "wide_bf16": bf16_round(rng.standard_normal((64, 128)) * np.exp(rng.standard_normal((64, 1)) * 3)),
+        # rows that sit exactly on the 4-bit lattice and rows with .5 ties
+        "lattice": np.array([rng.permutation(16).repeat(8) * 0.5 - 3.0 for _ in range(16)], dtype=np.float32),
+        "halves": (np.tile(np.arange(128) % 31, (16, 1)) * 0.5).astype(np.float32),
+        "constant": np.full((17, 128), -2.75, dtype=np.float32),
+    }
+    cases["mixed_const"] = np.concatenate([cases["gauss_bf16"][:20], cases["constant"][:5]])
+    for name, K in cases.items():
+        cache, meta = nk.build_cache(K, page_size=16, bits=4)
+        n, d = K.shape
+        codes = np.concatenate([_unpack_matrix(pg.packed, 16, d, 4)[: pg.valid_len] for pg in cache.pages])
+        packed = np.concatenate([np.frombuffer(pg.packed, dtype=np.uint8).reshape(16, d // 2)[: pg.valid_len] for pg in cache.pages])
+        scales = np.concatenate([pg.scales[: pg.valid_len] for pg in cache.pages])
+        zeros = np.concatenate([pg.zeros[: pg.valid_len] for pg in cache.pages])
+        quant[f"{name}/K"] = K
+        quant[f"{name}/codes"] = codes
+        quant[f"{name}/packed"] = packed
+        quant[f"{name}/scale"] = scales
+        quant[f"{name}/zero"] = zeros
+        quant[f"{name}/lo"] = np.stack([m.lo for m in meta])
+        quant[f"{name}/hi"] = np.stack([m.hi for m in meta])
+        # quantize_row on a few rows must agree with the vectorised build
+        for r in range(min(3, n)):
+            c, prm = nk.quantize_row(K[r])
+            quant[f"{name}/row{r}_codes"] = c
+            quant[f"{name}/row{r}_params"] = np.array([prm.scale, prm.zero])
+    quant["pack/arange16"] = np.frombuffer(nk.pack_codes(np.arange(16)), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "quant.npz"), **quant)
+
+    # ---------------------------------------------------------- quest
+    quest = {}
+    qi = 0
+    for n, budget, dt in [(2048, 512, "f32"), (1000, 0.25, "bf16"), (777, 100, "f32"), (1024, 0.5, "bf16"),
+                          (33, 16, "f32"), (20, 64, "bf16"), (1041, 300, "bf16")]:
+        K = rng.standard_normal((n, 128)).astype(np.float32)
+        q = (rng.standard_normal(128) / 0.5).astype(np.float32)
+        if dt == "bf16":
+            K, q = bf16_round(K), bf16_round(q)
+        meta = nk.build_page_metadata(K, 16)
+        scores = nk.quest_page_scores(q, meta)
+        sel = nk.select_quest(q, meta, budget, 16, n)
+        key = f"c{qi}"
+        quest[f"{key}/K"] = K
+        quest[f"{key}/q"] = q
+        quest[f"{key}/budget"] = np.array([budget], dtype=np.float64 if isinstance(budget, float) else np.int64)
+        quest[f"{key}/scores"] = scores
+        quest[f"{key}/selected"] = sel.indices
+        qi += 1
+    # tie handling: identical pages -> lower page wins
+    K = np.tile(bf16_round(rng.standard_normal((16, 128))), (8, 1))
+    q = bf16_round(rng.standard_normal(128))
+    meta = nk.build_page_metadata(K, 16)
+    quest["tie/K"] = K
+    quest["tie/q"] = q
+    quest["tie/budget"] = np.array([48], dtype=np.int64)
+    quest["tie/scores"] = nk.quest_page_scores(q, meta)
+    quest["tie/selected"] = nk.select_quest(q, meta, 48, 16, K.shape[0]).indices
+    np.savez_compressed(os.path.join(OUT, "quest.npz"), **quest)
+
+    # ---------------------------------------------------------- estimate
+    est = {}
+    for i, (n, dt) in enumerate([(300, "f32"), (512, "bf16"), (77, "f32")]):
+        K = rng.standard_normal((n, 128)).astype(np.float32)
+        q = (rng.standard_normal(128) * 2).astype(np.float32)
+        if dt == "bf16":
+            K, q = bf16_round(K), bf16_round(q)
+        cache, _ = nk.build_cache(K)
+        idx = np.sort(rng.choice(n, size=max(1, n // 3), replace=False))
+        sel = nk.TokenSelection.from_indices(idx, n)
+        r = nk.estimate_scores(q, cache, sel)
+        est[f"e{i}/K"] = K
+        est[f"e{i}/q"] = q
+        est[f"e{i}/idx"] = idx
+        est[f"e{i}/scores"] = r.scores
+        est[f"e{i}/bytes"] = np.array([r.bytes_touched])
+    np.savez_compressed(os.path.join(OUT, "estimate.npz"), **est)
+
+    # ---------------------------------------------------------- top-p
+    topp = {}
+    t = 0
+    for n in (1, 2, 16, 100, 1000, 2500):
+        for spread in (0.3, 1.0, 3.0, 8.0):
+            z = rng.standard_normal(n) * spread
+            w = np.exp(z - z.max())
+            w = w / w.sum()
+            for p in (0.0, 0.5, 0.9, 0.95, 0.99, 1.0):
+                out = nk.binary_search_top_p(w, nk.BinarySearchConfig(p=p))
+                topp[f"t{t}/w"] = w
+                topp[f"t{t}/p"] = np.array([p])
+                topp[f"t{t}/idx"] = out.selection.indices
+                topp[f"t{t}/threshold"] = np.array([out.threshold])
+                topp[f"t{t}/iterations"] = np.array([out.iterations])
+                topp[f"t{t}/cfg"] = np.array([1e-15, 64.0])
+                t += 1
+    specials = [
+        (np.array([0.3, 0.3, 0.2, 0.2]), 0.7, 1e-15, 64),
+        (np.array([0.3, 0.3, 0.2, 0.2]), 0.5, 1e-15, 64),
+        (np.array([0.6, 0.0, 0.4]), 1.0, 1e-15, 64),
+        (np.full(4, 0.25), 0.0, 1e-15, 64),
+        (np.full(8, 0.125), 0.3, 1e-15, 64),
+        (np.array([0.5, 0.25, 0.25]), 0.6, 1e-15, 64),
+    ]
+    z = rng.standard_normal(512)
+    w512 = np.exp(z - z.max()); w512 /= w512.sum()
+    specials += [(w512, 0.9, 1e-15, 1), (w512, 0.9, 1e6, 64), (w512, 0.9, 1e-4, 64), (w512, 0.99, 1e-15, 5)]
+    for w, p, eps, mi in specials:
+        out = nk.binary_search_top_p(w, nk.BinarySearchConfig(p=p, epsilon=eps, max_iters=mi))
+        topp[f"t{t}/w"] = w
+        topp[f"t{t}/p"] = np.array([p])
+        topp[f"t{t}/idx"] = out.selection.indices
+        topp[f"t{t}/threshold"] = np.array([out.threshold])
+        topp[f"t{t}/iterations"] = np.array([out.iterations])
+        topp[f"t{t}/cfg"] = np.array([eps, float(mi)])
+        t += 1
+    np.savez_compressed(os.path.join(OUT, "topp.npz"), **topp)
+
+    # ---------------------------------------------------------- attention
+    att = {}
+    for i, (n, dt) in enumerate([(500, "f32"), (64, "bf16")]):
+        K = rng.standard_normal((n, 128)).astype(np.float32)
+        V = rng.standard_normal((n, 128)).astype(np.float32)
+        q = (rng.standard_normal(128) * 1.5).astype(np.float32)
+        if dt == "bf16":
+            K, V, q = bf16_round(K), bf16_round(V), bf16_round(q)
+        w = nk.attention_weights(q, K)
+        idx = np.sort(rng.choice(n, size=n // 4, replace=False))
+        sel = nk.TokenSelection.from_indices(idx, n)
+        att[f"a{i}/K"], att[f"a{i}/V"], att[f"a{i}/q"], att[f"a{i}/idx"] = K, V, q, idx
+        att[f"a{i}/w"] = w
+        att[f"a{i}/out_renorm"] = nk.sparse_attention(w, V, sel, renormalize=True)
+        att[f"a{i}/out_plain"] = nk.sparse_attention(w, V, sel, renormalize=False)
+    np.savez_compressed(os.path.join(OUT, "attention.npz"), **att)
+
+    # ---------------------------------------------------------- pipeline
+    pipe = {}
+    configs = [
+        # name, n, G, selector, budget, p, tau, dtype
+        ("grouped_quest_f32", 1024, 4, "quest", 512, 0.95, 0.5, "f32"),
+        ("grouped_quest_bf16", 800, 4, "quest", 0.25, 0.95, 0.35, "bf16"),
+        ("head_full_bf16", 600, 1, "full", None, 0.9, 0.4, "bf16"),
+        ("head_quest_f32", 777, 1, "quest", 200, 0.8, 1.0, "f32"),
+        ("grouped_full_f32", 640, 2, "full", None, 0.99, 2.0, "f32"),
+    ]
+    for name, n, G, kind, budget, p, tau, dt in configs:
+        K = rng.standard_normal((n, 128)).astype(np.float32)
+        V = rng.standard_normal((n, 128)).astype(np.float32)
+        Q = (rng.standard_normal((G, 128)) / tau).astype(np.float32)
+        if dt == "bf16":
+            K, V, Q = bf16_round(K), bf16_round(V), bf16_round(Q)
+        sel = nk.SelectorConfig(kind=kind, budget=budget, page_size=16)
+        cfg = nk.PipelineConfig(selector=sel, prune=nk.BinarySearchConfig(p=p), group_map=nk.GroupMap(G))
+        if G == 1:
+            out, outcome, report = nk.run_head(Q[0], K, V, cfg)
+            outs, finals, b0 = out[None], [outcome.selection.indices], [report.b0]
+        else:
+            outs, outcomes, reports = nk.run_grouped(Q, K, V, cfg)
+            finals, b0 = [o.selection.indices for o in outcomes], [r.b0 for r in reports]
+        pipe[f"{name}/K"], pipe[f"{name}/V"], pipe[f"{name}/Q"] = K, V, Q
+        pipe[f"{name}/cfg"] = np.array([-1 if budget is None else budget, p, 1.0 if kind == "quest" else 0.0,
+                                        1.0 if isinstance(budget, float) else 0.0])
+        pipe[f"{name}/out"] = np.asarray(outs)
+        pipe[f"{name}/final"] = finals[0]
+        pipe[f"{name}/b0"] = np.array(b0)
+        for h, f in enumerate(finals):
+            assert np.array_equal(f, finals[0]) or G == 1
+    np.savez_compressed(os.path.join(OUT, "pipeline.npz"), **pipe)
+    print("golden vectors written to", OUT)
+
+
+if __name__ == "__main__":
+    main()
