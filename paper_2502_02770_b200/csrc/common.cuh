@@ -1,0 +1,128 @@
+// Shared device helpers for the Twilight sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "../../include/twilight.h"
+
+namespace tw {
+
+constexpr int kPage = 16;          // tokens per page (SelectorConfig.page_size, selectors.py:39)
+constexpr int kHeadDim = 128;      // d: Llama-3.1-8B / LongChat-7B head dim
+constexpr int kCodeBytes = kPage * kHeadDim / 2;      // 1024 B of packed nibbles per (page, kv head)
+constexpr int kQBlockBytes = kCodeBytes + kPage * 8;  // + fp32 scale[16] + fp32 zero[16] = 1152 B
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------- element types
+
+template <typename T> struct Elem;
+template <> struct Elem<float> {
+  static constexpr int kId = TW_F32;
+  __device__ __forceinline__ static float to_f(float x) { return x; }
+  __device__ __forceinline__ static float from_f(float x) { return x; }
+};
+template <> struct Elem<__nv_bfloat16> {
+  static constexpr int kId = TW_BF16;
+  __device__ __forceinline__ static float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+  __device__ __forceinline__ static __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
+};
+
+// 8 consecutive elements (16 B for bf16, 32 B for fp32) -> 8 floats
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&o)[8]) {
+  uint4 v = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o[2 * i] = __uint_as_float(w[i] << 16);
+    o[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+__device__ __forceinline__ void load8(const float* p, float (&o)[8]) {
+  float4 a = *reinterpret_cast<const float4*>(p);
+  float4 b = *reinterpret_cast<const float4*>(p + 4);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
+
+// streaming (read-once) 16-byte load that does not allocate in L1
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void cvt8(const uint4& v, const __nv_bfloat16*, float (&o)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o[2 * i] = __uint_as_float(w[i] << 16);
+    o[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+// ---------------------------------------------------------------- ordering keys
+
+// Monotone map fp32 -> u32: a < b  <=>  key(a) < key(b) (for non-NaN).
+__device__ __forceinline__ uint32_t f2key(float f) {
+  uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  uint32_t b = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  return __uint_as_float(b);
+}
+
+// ---------------------------------------------------------------- warp helpers
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// exp(z - m) for z <= m, accurate to a few fp32 ulp even when z - m is large:
+// the difference is formed exactly (two-sum) and the reduction uses a
+// Cody-Waite split of ln 2, so the only error is the degree-7 polynomial.
+__device__ __forceinline__ float exp_diff(float z, float m) {
+  float s = z - m;
+  float bb = s - z;
+  float err = (z - (s - bb)) + (-m - bb);
+  if (s < -103.0f) return 0.0f;
+  float k = rintf(s * 1.4426950408889634f);
+  float r = fmaf(-k, 0.693145751953125f, s);
+  r = fmaf(-k, 1.428606765330187e-06f, r);
+  r += err;
+  float p = 1.9841270e-4f;                 // 1/5040
+  p = fmaf(p, r, 1.3888889e-3f);           // 1/720
+  p = fmaf(p, r, 8.3333333e-3f);           // 1/120
+  p = fmaf(p, r, 4.1666667e-2f);           // 1/24
+  p = fmaf(p, r, 1.6666667e-1f);           // 1/6
+  p = fmaf(p, r, 0.5f);
+  p = fmaf(p, r, 1.0f);
+  p = fmaf(p, r, 1.0f);
+  int ki = (int)k;
+  if (ki < -125) return ldexpf(p, ki);     // gradual underflow
+  return p * __int_as_float((ki + 127) << 23);
+}
+
+// ---------------------------------------------------------------- launch check
+
+inline int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TW_OK : TW_ERR_CUDA;
+}
+
+}  // namespace tw

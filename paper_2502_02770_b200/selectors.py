@@ -1,0 +1,153 @@
+"""Candidate selectors with the reference signatures (nucleuskv/selectors.py).
+
+``quest_page_scores``, ``select_quest`` and ``group_union`` run on the B200
+kernels (tw_quest_scores / tw_select); ``select_full``/``resolve_budget`` are
+host arithmetic.  The channel-pruned and sink-window selectors are not on the
+accelerated path and raise NotImplementedError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+
+from . import _lib as L
+from .attention import TokenSelection
+
+SELECTOR_KINDS = ("full", "quest", "channel_pruned", "sink_window")
+
+
+@dataclass(frozen=True)
+class SelectorConfig:
+    """selectors.py:35-50."""
+    kind: str = "full"
+    budget: float | int | None = None
+    page_size: int = 16
+    top_channels: int | None = None
+    sink: int = 4
+    window: int = 64
+
+    def __post_init__(self) -> None:
+        if self.kind not in SELECTOR_KINDS:
+            raise ValueError(f"unknown selector kind {self.kind!r}")
+        if self.page_size < 1:
+            raise ValueError("page_size must be at least 1")
+        if self.sink < 0 or self.window < 0:
+            raise ValueError("sink and window must be non-negative")
+
+
+@dataclass(frozen=True)
+class GroupMap:
+    """selectors.py:53-69."""
+    group_size: int = 1
+
+    def __post_init__(self) -> None:
+        if self.group_size < 1:
+            raise ValueError("group_size must be at least 1")
+
+    def group_of(self, head: int) -> int:
+        return head // self.group_size
+
+    def groups(self, heads: int) -> int:
+        if heads % self.group_size != 0:
+            raise ValueError(f"{heads} heads not divisible into groups of {self.group_size}")
+        return heads // self.group_size
+
+
+def resolve_budget(budget: float | int, n: int) -> int:
+    """selectors.py:72-87: float fraction in (0, 1] (half-even round), int clamped to n."""
+    if isinstance(budget, bool):
+        raise ValueError("budget must be a number")
+    if isinstance(budget, float):
+        if not 0.0 < budget <= 1.0:
+            raise ValueError(f"fractional budget {budget} outside (0, 1]")
+        return max(1, min(n, round(budget * n)))
+    b = int(budget)
+    if b < 1:
+        raise ValueError("budget must select at least one token")
+    return min(b, n)
+
+
+def select_full(n: int, device="cuda") -> TokenSelection:
+    """selectors.py:90-94."""
+    if n < 1:
+        raise ValueError("context must contain at least one token")
+    return TokenSelection.from_indices(torch.arange(n, device=device), n)
+
+
+def quest_page_scores(q, metadata) -> torch.Tensor:
+    """fp64 page bounds, bit-identical to the reference (selectors.py:97-109)."""
+    from .quantcache import PageMetadataTable
+    if not isinstance(metadata, PageMetadataTable):
+        raise ValueError("metadata must come from build_page_metadata/build_cache of this package")
+    if len(metadata) == 0:
+        raise ValueError("no page metadata")
+    cache = metadata.cache
+    qv = torch.as_tensor(q, device=cache.device).to(cache.dtype).reshape(1, 1, L.HEAD_DIM).contiguous()
+    out = torch.empty(1, cache.max_pages, dtype=torch.float64, device=cache.device)
+    L.check(L.lib().tw_quest_scores(ctypes.byref(cache.struct()), L.ptr(qv), L.ptr(out), L.stream_handle()),
+            "tw_quest_scores")
+    return out[0, : len(metadata)]
+
+
+def select_quest(q, metadata, budget, page_size: int, n: int) -> TokenSelection:
+    """selectors.py:112-132 on the tw_select kernel (exact top-k, ties -> lower page)."""
+    from .decode import TwilightDecoder
+    from .quantcache import PageMetadataTable
+    expected = math.ceil(n / page_size)
+    if not isinstance(metadata, PageMetadataTable):
+        raise ValueError("metadata must come from build_page_metadata/build_cache of this package")
+    if len(metadata) and len(metadata) != expected:
+        raise ValueError(f"metadata covers {len(metadata)} pages, context of {n} needs {expected}")
+    if page_size != L.PAGE_SIZE:
+        raise ValueError("the B200 path uses 16-token pages")
+    cache = metadata.cache
+    b0 = resolve_budget(budget, n)
+    dec = TwilightDecoder(cache, "quest", budget=b0, p=1.0, head_page_bits=True)
+    qv = torch.as_tensor(q, device=cache.device).to(cache.dtype).reshape(1, 1, L.HEAD_DIM).contiguous()
+    dec.select(qv)
+    pages = dec.bufs.cand_pages[0, : int(dec.bufs.cand_count[0].item())].long()
+    tok = (pages[:, None] * L.PAGE_SIZE + torch.arange(L.PAGE_SIZE, device=pages.device)).reshape(-1)
+    return TokenSelection.from_indices(tok[tok < n], n)
+
+
+def group_union(selections) -> TokenSelection:
+    """Sorted union of the heads' selections (selectors.py:178-186)."""
+    if not selections:
+        raise ValueError("no selections to union")
+    n = selections[0].n
+    if any(s.n != n for s in selections):
+        raise ValueError("selections span different context sizes")
+    merged = torch.unique(torch.cat([s.indices for s in selections]))
+    return TokenSelection.from_indices(merged, n)
+
+
+def select_channel_pruned(*args, **kwargs):
+    raise NotImplementedError("channel-pruned selection is not on the B200 path (SURVEY.md 2.1)")
+
+
+def select_sink_window(*args, **kwargs):
+    raise NotImplementedError("sink-window selection is not on the B200 path (SURVEY.md 2.1)")
+
+
+def top_channels_by_magnitude(*args, **kwargs):
+    raise NotImplementedError("channel-pruned selection is not on the B200 path (SURVEY.md 2.1)")
+
+
+def build_selector(cfg: SelectorConfig, keys, metadata=None) -> Callable:
+    """selectors.py:189-209 for the accelerated kinds (full, quest)."""
+    n = int(keys.shape[0])
+    if cfg.kind == "full":
+        dev = keys.device if isinstance(keys, torch.Tensor) else "cuda"
+        return lambda q: select_full(n, dev)
+    if cfg.kind in ("channel_pruned", "sink_window"):
+        raise NotImplementedError(f"selector {cfg.kind!r} is not on the B200 path")
+    if cfg.budget is None:
+        raise ValueError(f"selector {cfg.kind!r} requires a budget")
+    if metadata is None:
+        raise ValueError("quest selector requires page metadata")
+    return lambda q: select_quest(q, metadata, cfg.budget, cfg.page_size, n)

@@ -1,0 +1,238 @@
+"""GPU parity of the batched decode kernels against the CPU oracle.
+
+K1 codes / packed bytes / params / metadata: bit-exact.  K2 page sets and
+union: bit-exact (and the fp64 page scores bit-identical to NumPy).  K3
+logits: fp32 tolerance; top-p sets: identical up to threshold ties (1e-6).
+K4/K5 outputs: 1e-4 relative (fp32) and bf16 inputs with fp32 accumulation.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import twilight_oracle as orc
+from tests.gpu_util import f2key_np, to_np, topp_set_ok
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2502_02770_b200 import _lib  # noqa: E402
+from paper_2502_02770_b200.decode import PagedKVCache, TwilightDecoder, pages_for  # noqa: E402
+from paper_2502_02770_b200.workload import make_batch, tau_schedule  # noqa: E402
+
+DTYPES = [torch.float32, torch.bfloat16]
+
+
+def _cache(B, H, G, n, dtype, lengths, seed=0, tau=1.0, page_local=False, extra_pages=2):
+    batch = make_batch(B, H, G, n, dtype, tau=tau, seed=seed, page_local=page_local)
+    cache = PagedKVCache(B, H, G, max_pages=pages_for(n) + extra_pages, dtype=dtype)
+    cache.prefill(batch.K, batch.V, lengths)
+    return cache, batch
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_k1_bulk_quantization_bit_exact(dtype):
+    B, H, G = 2, 3, 1
+    cache, _ = _cache(B, H, G, 300, dtype, [300, 177], seed=1)
+    for b in range(B):
+        for h in range(H):
+            K = to_np(cache.unit_keys(b, h))
+            codes, scale, zero = orc.quantize_rows(K)
+            packed, sc, zr = cache.unit_quant(b, h)
+            np.testing.assert_array_equal(packed.cpu().numpy(), orc.pack_nibbles(codes))
+            np.testing.assert_array_equal(sc.cpu().numpy(), scale.astype(np.float32))
+            np.testing.assert_array_equal(zr.cpu().numpy(), zero.astype(np.float32))
+            lo, hi = cache.unit_meta(b, h)
+            olo, ohi = orc.page_bounds(K)
+            np.testing.assert_array_equal(to_np(lo), olo.astype(np.float32))
+            np.testing.assert_array_equal(to_np(hi), ohi.astype(np.float32))
+            assert float(cache.kabsmax[b, h]) == float(np.abs(K).max())
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_k1_append_equals_bulk(dtype):
+    B, H, G, n = 2, 2, 4, 300
+    lengths = [300, 177]
+    full, batch = _cache(B, H, G, n, dtype, lengths, seed=2)
+    inc = PagedKVCache(B, H, G, max_pages=full.max_pages, dtype=dtype)
+    tail = 21
+    inc.prefill(batch.K, batch.V, [l - tail for l in lengths])
+    for i in range(tail):
+        pos = torch.tensor([l - tail + i for l in lengths], dtype=torch.int32, device="cuda")
+        idx = pos.long().view(B, 1, 1, 1).expand(B, H, 1, 128)
+        k_new = torch.gather(batch.K, 2, idx).squeeze(2).contiguous()
+        v_new = torch.gather(batch.V, 2, idx).squeeze(2).contiguous()
+        inc.append(k_new, v_new)
+    torch.cuda.synchronize()
+    assert inc.seq_lens.tolist() == lengths
+    for b in range(B):
+        for h in range(H):
+            for a, c in zip(inc.unit_quant(b, h), full.unit_quant(b, h)):
+                assert torch.equal(a, c)
+            for a, c in zip(inc.unit_meta(b, h), full.unit_meta(b, h)):
+                assert torch.equal(a, c)
+            assert torch.equal(inc.unit_keys(b, h), full.unit_keys(b, h))
+            assert torch.equal(inc.unit_values(b, h), full.unit_values(b, h))
+    assert torch.equal(inc.kabsmax, full.kabsmax)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("page_local", [False, True])
+def test_k2_quest_pages_bit_exact(dtype, page_local):
+    B, H, G, n = 2, 2, 4, 1000
+    lengths = [1000, 777]
+    cache, batch = _cache(B, H, G, n, dtype, lengths, seed=3, tau=0.5, page_local=page_local)
+    budget = 256
+    dec = TwilightDecoder(cache, "quest", budget=budget, p=0.95, head_page_bits=True)
+    q = batch.q.contiguous()
+    dec.select(q)
+    # exact fp64 page bounds, bit-identical to NumPy
+    import ctypes
+    scores = torch.empty(B * H * G, cache.max_pages, dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().tw_quest_scores(ctypes.byref(cache.struct()), _lib.ptr(q), _lib.ptr(scores),
+                                          _lib.stream_handle()), "tw_quest_scores")
+    torch.cuda.synchronize()
+    bits = dec.bufs.head_page_bits.cpu().numpy().view(np.uint32)
+    for b in range(B):
+        for h in range(H):
+            K = to_np(cache.unit_keys(b, h))
+            lo, hi = orc.page_bounds(K)
+            u = b * H + h
+            heads = []
+            for g in range(G):
+                qh = to_np(q[b, h * G + g])
+                want = orc.quest_select_pages(qh, lo, hi, budget, lengths[b])
+                np.testing.assert_array_equal(scores[u * G + g, : lo.shape[0]].cpu().numpy(),
+                                              orc.quest_scores(qh, lo, hi))
+                got = np.flatnonzero(np.unpackbits(bits[u * G + g].view(np.uint8), bitorder="little"))
+                np.testing.assert_array_equal(got, want)
+                heads.append(want)
+            cnt = int(dec.bufs.cand_count[u])
+            np.testing.assert_array_equal(dec.bufs.cand_pages[u, :cnt].cpu().numpy(), orc.union_sorted(heads))
+
+
+def test_k2_ties_go_to_the_lower_page():
+    B, H, G = 1, 1, 1
+    base = make_batch(1, 1, 1, 16, torch.bfloat16, seed=4)
+    K = base.K.repeat(1, 1, 8, 1)  # eight identical pages
+    cache = PagedKVCache(B, H, G, max_pages=8, dtype=torch.bfloat16)
+    cache.prefill(K, K, [128])
+    dec = TwilightDecoder(cache, "quest", budget=48, p=0.9)
+    dec.select(base.q[:, :1].contiguous())
+    assert dec.bufs.cand_pages[0, : int(dec.bufs.cand_count[0])].tolist() == [0, 1, 2]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("G", [1, 4])
+def test_k3_estimate_topp_and_k4_attention(dtype, G):
+    B, H, n = 2, 2, 1500
+    lengths = [1500, 1111]
+    tau = tau_schedule(H, (0.3, 1.0))
+    cache, batch = _cache(B, H, G, n, dtype, lengths, seed=5 + G, tau=tau)
+    p = 0.95
+    dec = TwilightDecoder(cache, "quest", budget=512, p=p)
+    q = batch.q.contiguous()
+    out = dec.forward(q)
+    torch.cuda.synchronize()
+    bufs = dec.bufs
+    T = cache.max_pages * 16
+    exact, tolerant = 0, 0
+    for b in range(B):
+        for h in range(H):
+            u = b * H + h
+            K = to_np(cache.unit_keys(b, h))
+            V = to_np(cache.unit_values(b, h))
+            codes, scale, zero = orc.quantize_rows(K)
+            ncand = int(bufs.cand_count[u])
+            pages = bufs.cand_pages[u, :ncand].cpu().numpy()
+            cand = orc.pages_to_tokens(pages, lengths[b])
+            pos = (pages[:, None] * 16 + np.arange(16)).reshape(-1)
+            valid = pos < lengths[b]
+            head_sets = []
+            for g in range(G):
+                qh = to_np(q[b, h * G + g])
+                z_gpu = bufs.logits[u, g, : ncand * 16].cpu().numpy()
+                assert np.all(np.isneginf(z_gpu[~valid]))
+                z_gpu = z_gpu[valid]
+                z_ref = orc.estimate_logits(qh, codes, scale, zero, cand)
+                scale_ref = np.abs(qh).sum() * np.abs(K).max() / np.sqrt(128)
+                np.testing.assert_allclose(z_gpu, z_ref, rtol=0, atol=2e-6 * scale_ref + 1e-6)
+                # isolated pruner: the oracle softmax + search on the GPU's own logits
+                thr = np.uint32(bufs.head_thr[u * G + g].item() & 0xFFFFFFFF)
+                sel = np.flatnonzero(f2key_np(z_gpu) >= thr)
+                w = orc.softmax64(z_gpu)
+                ok, why = topp_set_ok(sel, w, p)
+                assert ok, f"unit {u} head {g}: {why}"
+                exact += why == "equal"
+                tolerant += why != "equal"
+                head_sets.append(cand[sel])
+                assert int(bufs.head_stats[u * G + g, 0]) == sel.size
+            final = orc.union_sorted(head_sets)
+            cnt = int(bufs.final_count[u])
+            np.testing.assert_array_equal(bufs.final_idx[u, :cnt].cpu().numpy(), final)
+            # attention over the identical final set (reference: pipeline.py:366-375)
+            for g in range(G):
+                qh = to_np(q[b, h * G + g])
+                w = orc.full_weights(qh, K)
+                want = orc.subset_attention(w, V, final, w[final].sum() > 0)
+                got = to_np(out[b, h * G + g])
+                np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-4 * np.abs(want).max())
+    assert exact >= tolerant  # near-threshold ties are the exception
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_k3_full_selector(dtype):
+    B, H, G, n = 1, 2, 1, 3000
+    cache, batch = _cache(B, H, G, n, dtype, [n], seed=9, tau=0.25)
+    dec = TwilightDecoder(cache, "full", p=0.9)
+    q = batch.q.contiguous()
+    out = dec.forward(q)
+    torch.cuda.synchronize()
+    for h in range(H):
+        assert int(dec.bufs.cand_count[h]) == pages_for(n)
+        K, V = to_np(cache.unit_keys(0, h)), to_np(cache.unit_values(0, h))
+        cnt = int(dec.bufs.final_count[h])
+        final = dec.bufs.final_idx[h, :cnt].cpu().numpy()
+        z = dec.bufs.logits[h, 0, :n].cpu().numpy()
+        ok, why = topp_set_ok(final, orc.softmax64(z), 0.9)
+        assert ok, why
+        w = orc.full_weights(to_np(q[0, h]), K)
+        want = orc.subset_attention(w, V, final, True)
+        np.testing.assert_allclose(to_np(out[0, h]), want, rtol=1e-4, atol=1e-4 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_k5_dense_attention(dtype):
+    B, H, G, n = 2, 2, 4, 2100
+    lengths = [2100, 1337]
+    cache, batch = _cache(B, H, G, n, dtype, lengths, seed=11, tau=0.7)
+    dec = TwilightDecoder(cache, "full", p=1.0)
+    q = batch.q.contiguous()
+    out = dec.dense(q)
+    torch.cuda.synchronize()
+    for b in range(B):
+        for h in range(H):
+            K, V = to_np(cache.unit_keys(b, h)), to_np(cache.unit_values(b, h))
+            for g in range(G):
+                w = orc.full_weights(to_np(q[b, h * G + g]), K)
+                want = w @ V
+                np.testing.assert_allclose(to_np(out[b, h * G + g]), want, rtol=1e-4,
+                                           atol=1e-4 * np.abs(want).max())
+
+
+def test_decode_step_fused_matches_staged():
+    B, H, G, n = 2, 2, 4, 900
+    dtype = torch.bfloat16
+    a, batch = _cache(B, H, G, n, dtype, [900, 640], seed=13, tau=0.5)
+    c, _ = _cache(B, H, G, n, dtype, [900, 640], seed=13, tau=0.5)
+    q = batch.q.contiguous()
+    da = TwilightDecoder(a, "quest", budget=256, p=0.95)
+    dc = TwilightDecoder(c, "quest", budget=256, p=0.95)
+    out_a = da.step(q, batch.k_new, batch.v_new)
+    c.append(batch.k_new, batch.v_new)
+    out_c = dc.forward(q)
+    torch.cuda.synchronize()
+    assert a.seq_lens.tolist() == [901, 641]
+    assert torch.equal(out_a, out_c)
