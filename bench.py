@@ -1,0 +1,544 @@
+"""Benchmark of the B200 Twilight decode-attention path.
+
+Metric (BASELINE.json): sparse decode-attention microseconds per layer and
+achieved HBM GB/s.  One "step" = one decode step of ONE attention layer for
+the whole batch: K1 append of the new token, K2 Quest selection + GQA union,
+K3 INT4 estimate + top-p + group union, K4 sparse attention (+ split-KV merge).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+N>1 is launched by torchrun (one process per GPU, NCCL); C1/C2/C4/C5-style
+configs are batch-sharded (weak scaling: every rank owns its own batch, no
+data-path collective), C3 is KV-head-sharded with one NCCL all-gather of the
+per-head outputs.  Timing: CUDA events on the launching stream, W warm-up
+steps, a barrier + synchronize on both sides of exactly K steps, max over
+ranks.  Inputs larger than L2: steps rotate over `layers` independent layer
+caches (each bigger than the 126 MB L2).  Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+# ----------------------------------------------------------------------------- configs
+# n = context length attended (after the append), B per GPU, heads, selector, budget (tokens), p
+CONFIGS = {
+    "C1": dict(desc="single-layer decode, Llama-3.1-8B head shape (32 q / 8 kv, d=128), batch 1, ctx 8k, "
+                    "Quest page 16, p=0.95, random K/V", B=1, H=8, G=4, n=8192, selector="quest", budget=2048,
+               p=0.95, layers=16, shard="batch"),
+    "C2": dict(desc="Llama-3.1-8B layer shape, batch 16, ctx 32k, Quest budget 8192 + top-p p=0.95, bf16",
+               B=16, H=8, G=4, n=32768, selector="quest", budget=8192, p=0.95, layers=4, shard="batch"),
+    "C3": dict(desc="LongChat-7B MHA shape (32 heads, d=128), batch 8, ctx 128k, full selector + top-p p=0.9, "
+                    "head-sharded", B=8, H=32, G=1, n=131072, selector="full", budget=None, p=0.9, layers=2,
+               shard="head"),
+    "C5": dict(desc="Llama-3.1-8B shape, batch 32, ctx 128k, Quest n/4 + top-p (p sweep point 0.9), "
+                    "focused vs diffuse heads", B=32, H=8, G=4, n=131072, selector="quest", budget=32768, p=0.9,
+               layers=2, shard="batch"),
+}
+TAUS = (0.25, 0.5, 1.0, 2.0)  # per-KV-head temperatures, cycled: focused .. diffuse
+METRIC = "sparse decode-attn us/layer & achieved HBM GB/s at 32k-128k ctx, 1/2/4/8 GPU"
+
+
+def load_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json: 1 Gi bf16 copy, read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        rows = []
+        for l in self.lines:
+            parts = [x.strip() for x in l.split(",")]
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:]))
+            except Exception:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for _, _, flags in rows:
+            for nm, fl in zip(names, flags):
+                if fl.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [r[0] for r in rows if r[0] > 500] or [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def dist_setup(gpus: int):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def algorithmic_bytes(cfg, dec, n, elem=2):
+    """HBM bytes one step MUST move, from the step's actual
+    candidate pages U and final sets B1 (read back after timing)."""
+    H, G, B = cfg["H_local"], cfg["G"], cfg["B"]
+    units = B * H
+    d = 128
+    P = math.ceil(n / 16)
+    bufs = dec.bufs
+    U = bufs.cand_count.sum().item()  # candidate pages over all units
+    F = bufs.final_count.sum().item()  # surviving tokens over all units
+    k1 = units * (2 * 2 * d * elem + d // 2 + 8 + 2 * 2 * d * elem)          # read k,v; write k,v,codes,params; meta RMW
+    k2 = units * (P * 2 * d * elem + G * d * elem + 4 * P) if cfg["selector"] == "quest" else 0
+    k3a = U * 1152                                                            # INT4 codes + fp32 scale/zero per page
+    k3bc = 4 * F                                                              # final index list
+    k4 = F * (2 * d * elem + 4) + units * G * d * (elem + 4)                  # gathered K,V rows + q + out
+    dense = units * n * 2 * d * elem + units * G * d * (elem + 4)
+    return {"K1_append": k1, "K2_select": k2, "K3a_estimate": k3a, "K3bc_topp": k3bc, "K4_attention": k4,
+            "step": k1 + k2 + k3a + k3bc + k4, "K5_dense": dense, "cand_pages": U, "final_tokens": F}
+
+
+def run_ours(args, cfg):
+    from paper_2502_02770_b200.decode import DecodeBuffers, PagedKVCache, TwilightDecoder, pages_for
+    from paper_2502_02770_b200.workload import make_batch, tau_schedule
+
+    rank, world, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local if world > 1 else 0)
+    B, H, G, n = cfg["B"], cfg["H"], cfg["G"], cfg["n"]
+    if cfg["shard"] == "head":
+        assert H % world == 0, "heads must divide over ranks"
+        H_local = H // world
+    else:
+        H_local = H
+    cfg = dict(cfg, H_local=H_local)
+    dtype = torch.bfloat16
+    L = args.layers or cfg["layers"]
+    max_pages = pages_for(n)
+    taus = tau_schedule(H, TAUS)[rank * H_local:(rank + 1) * H_local] if cfg["shard"] == "head" else tau_schedule(H, TAUS)
+    seed0 = 1234 + 7919 * rank
+
+    caches, decs = [], []
+    shared = None
+    for layer in range(L):
+        cache = PagedKVCache(B, H_local, G, max_pages, dtype=dtype, device=dev)
+        batch = make_batch(B, H_local, G, n, dtype, tau=taus, seed=seed0 + layer, device=dev)
+        cache.prefill(batch.K[:, :, : n - 1], batch.V[:, :, : n - 1])  # the step appends token n-1
+        del batch
+        dec = TwilightDecoder(cache, cfg["selector"], budget=cfg["budget"], p=cfg["p"], bufs=shared)
+        shared = dec.bufs
+        caches.append(cache)
+        decs.append(dec)
+        torch.cuda.synchronize()
+    step_in = make_batch(B, H_local, G, 16, dtype, tau=taus, seed=seed0 + 999, device=dev)
+    q, k_new, v_new = step_in.q.contiguous(), step_in.k_new.contiguous(), step_in.v_new.contiguous()
+    positions = torch.full((B,), n - 1, dtype=torch.int32, device=dev)
+    out = torch.empty(B, H_local * G, 128, dtype=torch.float32, device=dev)
+    gathered = torch.empty(world, B, H_local * G, 128, dtype=torch.float32, device=dev) if (
+        cfg["shard"] == "head" and world > 1) else None
+
+    def step_once(i, which=None):
+        dec = decs[i % L]
+        if which is None:
+            dec.step(q, k_new, v_new, positions, out)
+        if gathered is not None:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(gathered, out)
+
+    # --- CUDA graphs: one graph per layer for the fused step (launch-bound otherwise)
+    graphs = []
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for i in range(L):  # warm the launch path (cudaFuncSetAttribute etc.) outside capture
+            decs[i].step(q, k_new, v_new, positions, out)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    for i in range(L):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            decs[i].step(q, k_new, v_new, positions, out)
+        graphs.append(g)
+    torch.cuda.synchronize()
+
+    def replay(i):
+        graphs[i % L].replay()
+        if gathered is not None:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(gathered, out)
+
+    for i in range(args.warmup):
+        replay(i)
+    torch.cuda.synchronize()
+    barrier(world)
+
+    # --- main timed region: exactly K steps
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local if world > 1 else 0) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(args.steps):
+            replay(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms_local, world)
+    clocks = clk.summary()
+
+    # --- per-stage breakdown: each stage captured in its own CUDA graph, events between replays
+    stage_names = ["K1_append", "K2_select", "K3a_estimate", "K3bc_topp", "K4_attention"]
+    stage_fns = lambda dec: [lambda: dec.cache.append(k_new, v_new, positions), lambda: dec.select(q),
+                             lambda: dec.estimate(q), lambda: dec.topp(), lambda: dec.attend(q, out)]
+    stage_graphs = []
+    for i in range(L):
+        row = []
+        for fn in stage_fns(decs[i]):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            row.append(g)
+        stage_graphs.append(row)
+    stage_ms = {k: 0.0 for k in stage_names}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stage_names) + 1)]
+    reps = max(3, min(args.steps, 10))
+    for i in range(reps + 1):
+        ev[0].record(stream)
+        for j, g in enumerate(stage_graphs[i % L]):
+            g.replay()
+            ev[j + 1].record(stream)
+        torch.cuda.synchronize()
+        if i == 0:
+            continue
+        for j, k in enumerate(stage_names):
+            stage_ms[k] += ev[j].elapsed_time(ev[j + 1]) / reps
+
+    # --- dense decode attention (K5) on the same caches: the speedup baseline
+    dense_graphs = []
+    for i in range(L):
+        decs[i].dense(q, out)
+    torch.cuda.synchronize()
+    for i in range(L):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            decs[i].dense(q, out)
+        dense_graphs.append(g)
+    for i in range(args.warmup):
+        dense_graphs[i % L].replay()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(args.steps):
+        dense_graphs[i % L].replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dense_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+
+    # --- end to end through the C-ABI step with host buffers (pinned), H2D + D2H inside the timed region
+    q_h = q.cpu().pin_memory()
+    k_h, v_h = k_new.cpu().pin_memory(), v_new.cpu().pin_memory()
+    out_h = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    q_d, k_d, v_d = torch.empty_like(q), torch.empty_like(k_new), torch.empty_like(v_new)
+    e2e_graphs = []
+    for i in range(L):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            decs[i].step(q_d, k_d, v_d, positions, out)
+        e2e_graphs.append(g)
+    for i in range(args.warmup):
+        q_d.copy_(q_h, non_blocking=True)
+        e2e_graphs[i % L].replay()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0.record(stream)
+    for i in range(args.steps):
+        q_d.copy_(q_h, non_blocking=True)
+        k_d.copy_(k_h, non_blocking=True)
+        v_d.copy_(v_h, non_blocking=True)
+        e2e_graphs[i % L].replay()
+        if gathered is not None:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(gathered, out)
+        out_h.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    h2d = q.numel() * q.element_size() + k_new.numel() * k_new.element_size() * 2
+    d2h = out.numel() * out.element_size()
+
+    # --- bytes, roofline, stats
+    dec0 = decs[(args.steps - 1) % L]
+    ab = algorithmic_bytes(cfg, dec0, n)
+    peak, peak_src = load_peak()
+    kernel_gbs = {k: (ab[k] / (stage_ms[k] * 1e-3) / 1e9 if stage_ms[k] > 0 and ab[k] else None) for k in stage_names}
+    dominant = max(stage_names, key=lambda k: stage_ms[k])
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(args.config, {}).get(dominant)
+        except Exception:
+            traffic = None
+    stats = dec0.stats()
+    b1 = stats.b1.float()
+    step_bytes_all = sum_over_ranks(ab["step"], world)
+    achieved_step = step_bytes_all / world / (ms * 1e-3) / 1e9  # per GPU
+    res = {
+        "metric": METRIC,
+        "value": round(ms * 1e3, 2),
+        "unit": "us/layer",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 5),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic: K,V iid N(0,1) bf16, q N(0,1)/tau per KV head (tau cycles 0.25,0.5,1,2), seeded",
+        "config": {"workload": cfg["desc"], "config_id": args.config, "batch_per_gpu": cfg["B"],
+                   "global_batch": cfg["B"] * (world if cfg["shard"] == "batch" else 1), "ctx": n,
+                   "kv_heads": H, "kv_heads_per_gpu": H_local, "group_size": G, "selector": cfg["selector"],
+                   "budget_tokens": cfg["budget"], "p": cfg["p"],
+                   "parallelism": f"{'batch' if cfg['shard'] == 'batch' else 'kv-head'}-sharded x{world}",
+                   "l2": f"steps rotate over {L} layer caches of {caches[0].k_cache.numel() * 4 / 1e9:.2f} GB each "
+                         "(K+V+INT4+meta >> 126 MB L2)", "cuda_graphs": True},
+        "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us/layer", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "tw_decode_step C-ABI call (captured), q/k_new/v_new from pinned host, out to pinned host"},
+        "gpu_launches": (8 if cfg["selector"] == "quest" else 7) * args.steps,
+        "roofline": {"bound": "hbm", "kernel": dominant,
+                     "achieved": round(kernel_gbs[dominant], 1) if kernel_gbs[dominant] else None,
+                     "peak": peak, "unit": "GB/s",
+                     "frac": round(kernel_gbs[dominant] / peak, 4) if kernel_gbs[dominant] else None,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": ab[dominant]},
+        "step_roofline": {"algorithmic_bytes": ab["step"], "achieved_gbs_per_gpu": round(achieved_step, 1),
+                          "frac": round(achieved_step / peak, 4)},
+        "kernels_us": {k: round(v * 1e3, 2) for k, v in stage_ms.items()},
+        "kernels_gbs": {k: (round(v, 1) if v else None) for k, v in kernel_gbs.items()},
+        "algorithmic_bytes": {k: ab[k] for k in stage_names},
+        "dense_us_per_layer": round(dense_ms * 1e3, 2),
+        "dense_gbs": round(ab["K5_dense"] / (dense_ms * 1e-3) / 1e9, 1),
+        "speedup_vs_dense": round(dense_ms / ms, 3),
+        "budgets": {"cand_tokens_mean_per_unit": round(ab["cand_pages"] * 16 / (B * H_local), 1),
+                    "final_tokens_mean_per_unit": round(ab["final_tokens"] / (B * H_local), 1),
+                    "head_b1_min": int(b1.min().item()), "head_b1_max": int(b1.max().item()),
+                    "head_b1_mean": round(float(b1.mean().item()), 1)},
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(cfg, n, samples=args.cpu_units)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- CPU legs (oracle port)
+
+def _unit_arrays(cfg, n, h, seed):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    K = rng.standard_normal((n, 128)).astype(np.float32)
+    V = rng.standard_normal((n, 128)).astype(np.float32)
+    tau = TAUS[h % len(TAUS)]
+    Q = (rng.standard_normal((cfg["G"], 128)) / tau).astype(np.float32)
+    # bf16-representable values, as the GPU sees them
+    def bf(x):
+        a = x.view(np.uint32).astype(np.uint64)
+        return (((a + 0x7FFF + ((a >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)).view(np.float32)
+    return bf(K), bf(V), bf(Q)
+
+
+def _cpu_unit(args):
+    """One (sequence, kv head) unit of the reference hot path on the CPU
+    oracle: append (quantize one row + page bounds update) then
+    select -> union -> estimate -> softmax -> threshold search -> union ->
+    attention, with the cache prebuilt (pipeline.py:306-360 with cache=)."""
+    cfg, n, h, seed, prepared_cache = args
+    import numpy as np
+    from oracle import twilight_oracle as orc
+    K, V, Q, prep = prepared_cache
+    t0 = time.perf_counter()
+    orc.quantize_rows(K[-1])          # K1 for the appended row
+    orc.page_bounds(K[-16:])          # and its page's bounds
+    orc.decode_unit(Q, K, V, selector=cfg["selector"], budget=cfg["budget"] or 1.0, p=cfg["p"],
+                    prepared=prep)
+    return time.perf_counter() - t0
+
+
+_POOL_STATE = {}
+
+
+def _pool_init(cfg, n, seed):
+    import numpy as np
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import twilight_oracle as orc
+    K, V, Q = _unit_arrays(cfg, n, seed % len(TAUS), seed)
+    _POOL_STATE["unit"] = (K, V, Q, orc.prepare_unit(K))
+    _POOL_STATE["cfg"] = cfg
+    _POOL_STATE["n"] = n
+
+
+def _pool_task(i):
+    cfg, n = _POOL_STATE["cfg"], _POOL_STATE["n"]
+    return _cpu_unit((cfg, n, i, 0, _POOL_STATE["unit"]))
+
+
+def cpu_baseline(cfg, n, samples=8):
+    """Oracle port, 1 thread, `samples` units of this workload; extrapolated
+    to the whole batch (units = B * H_kv)."""
+    import numpy as np
+    from oracle import twilight_oracle as orc
+    units = cfg["B"] * cfg["H_local"]
+    times = []
+    for s in range(samples):
+        K, V, Q = _unit_arrays(cfg, n, s, 100 + s)
+        prep = orc.prepare_unit(K)
+        times.append(_cpu_unit((cfg, n, s, 0, (K, V, Q, prep))))
+    per_unit = statistics.mean(times)
+    return {"value": round(per_unit * units * 1e6, 1), "unit": "us/layer", "cores": 1, "kind": "port",
+            "sample": f"{samples} of {units} (sequence, kv-head) units at ctx {n}, oracle/twilight_oracle.py "
+                      f"(NumPy restatement of nucleuskv), 1 thread, cache prebuilt, extrapolated x{units / samples:.1f}",
+            "seconds_per_unit": round(per_unit, 4)}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference algorithm (oracle port; the reference
+    is pure Python and cannot be compiled into oracle/_ref) on all host cores,
+    rank 0 only; each step = one unit per worker, extrapolated to the batch."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    n = cfg["n"]
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    H_local = cfg["H"] // world if cfg["shard"] == "head" else cfg["H"]
+    units = cfg["B"] * H_local * (world if cfg["shard"] == "batch" else 1)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_pool_init, initargs=(cfg, n, 4242)) as pool:
+        for _ in range(args.warmup):
+            pool.map(_pool_task, range(cores))
+        walls = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            pool.map(_pool_task, range(cores))
+            walls.append(time.perf_counter() - t0)
+    per_step = statistics.mean(walls) * units / cores  # seconds for the whole layer
+    value = round(per_step * 1e6, 1)
+    res = {"metric": METRIC, "value": value, "unit": "us/layer", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(per_step * 1e3, 3), "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (NumPy)", "data": "synthetic, seeded",
+           "impl": "reference",
+           "config": {"workload": cfg["desc"], "config_id": args.config},
+           "cpu_baseline": {"value": value, "unit": "us/layer", "cores": cores, "kind": "port",
+                            "sample": f"each step: {cores} (sequence, kv-head) units at ctx {n} in parallel "
+                                      f"(one per core), extrapolated to {units} units"},
+           "e2e": {"value": value, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--cpu-units", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = dict(CONFIGS[args.config])
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -37,6 +37,7 @@ extern "C" {
 
 #define TW_PAGE_SIZE 16
 #define TW_QBLOCK_BYTES 1152
+#define TW_DEFAULT_CHUNK 256 /* tokens per sparse-attention work item */
 
 /* Status codes; the shim maps them to the reference's exceptions
  * (attention.py:30-36, pruner.py:67-76, quantcache.py:246-267). */
@@ -73,7 +74,7 @@ typedef struct tw_decode_params {
   int32_t selector;     /* tw_selector: full (selectors.py:90-94) or quest (:112-132) */
   int32_t budget_pages; /* ceil(B0 / 16), B0 = resolve_budget(...) (selectors.py:72-87, :127) */
   double p;             /* top-p mass target, BinarySearchConfig.p (pruner.py:35) */
-  int32_t chunk_tokens; /* sparse-attention work-item size (0 = default 64) */
+  int32_t chunk_tokens; /* sparse-attention work-item size (0 = TW_DEFAULT_CHUNK) */
   int32_t renormalize;  /* must be 1 on this path (PipelineConfig.renormalize_output, pipeline.py:58) */
 } tw_decode_params;
 
@@ -94,6 +95,10 @@ typedef struct tw_decode_buffers {
   uint32_t* counters;       /* [8]               device-side counters (zeroed by tw_select) */
   float* partials;          /* [max_items][G][d+2] split-KV partial (o[d], m, l) */
   uint32_t* head_page_bits; /* optional [Hq][ceil(max_pages/32)] per-head Quest page sets */
+  uint32_t* sel_bits;       /* [Hq][T/32]        per-head pruned set over candidate positions */
+  int32_t* unit_done;       /* [U]               completion counters (zeroed by the library) */
+  int32_t* band_idx;        /* [Hq][max_pages]   Quest pages in the fp32 filter's ambiguous band */
+  double* band_scores;      /* [Hq][max_pages]   their exact fp64 bounds */
   int64_t max_items;
 } tw_decode_buffers;
 

@@ -337,8 +337,16 @@ def subset_attention(w, V, idx, renormalize: bool) -> np.ndarray:
 # one unit end to end (the hot half of run_grouped / run_head)
 
 
+def prepare_unit(K, page_size: int = PAGE_SIZE):
+    """The cache the reference builds once per context (build_cache,
+    quantcache.py:178-235): page bounds + per-row INT4 codes/params."""
+    lo, hi = page_bounds(K, page_size)
+    codes, scale, zero = quantize_rows(K)
+    return lo, hi, codes, scale, zero
+
+
 def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.95,
-                page_size: int = PAGE_SIZE, renormalize: bool = True, logits_override=None):
+                page_size: int = PAGE_SIZE, renormalize: bool = True, logits_override=None, prepared=None):
     """run_grouped's hot path for one KV head (pipeline.py:306-360):
 
     per-head Quest (selectors.py:112-132) -> group union (:338) -> per-head
@@ -349,14 +357,14 @@ def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.9
     per test_pipeline.py:232-241).  ``selector`` is "quest" or "full".
 
     ``logits_override`` (G, |union|) replaces the INT4 estimate, so a test
-    can feed the GPU's logits to the oracle's softmax + search.
-    Returns a dict with every intermediate.
+    can feed the GPU's logits to the oracle's softmax + search;
+    ``prepared`` = prepare_unit(K) reuses a prebuilt cache (the reference's
+    cache=/metadata= arguments).  Returns a dict with every intermediate.
     """
     Q = np.atleast_2d(np.asarray(Q))
     n = K.shape[0]
     G = Q.shape[0]
-    lo, hi = page_bounds(K, page_size)
-    codes, scale, zero = quantize_rows(K)
+    lo, hi, codes, scale, zero = prepared if prepared is not None else prepare_unit(K, page_size)
     if selector == "full":
         head_pages = [np.arange(lo.shape[0]) for _ in range(G)]
     elif selector == "quest":

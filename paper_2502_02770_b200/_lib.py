@@ -13,12 +13,13 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libtwilight.so")
+LIB_PATH = os.environ.get("TW_LIB_PATH") or os.path.join(HERE, "_lib", "libtwilight.so")
 
 TW_OK, TW_ERR_INVALID, TW_ERR_INDEX, TW_ERR_DEGENERATE, TW_ERR_CUDA = range(5)
 TW_F32, TW_BF16 = 0, 1
 TW_SELECT_FULL, TW_SELECT_QUEST = 0, 1
 PAGE_SIZE = 16
+DEFAULT_CHUNK = 256
 QBLOCK_BYTES = 1152
 HEAD_DIM = 128
 
@@ -59,7 +60,9 @@ class TwDecodeBuffers(ctypes.Structure):
         ("logits", ctypes.c_void_p), ("head_max", ctypes.c_void_p), ("head_thr", ctypes.c_void_p),
         ("head_stats", ctypes.c_void_p), ("final_idx", ctypes.c_void_p), ("final_count", ctypes.c_void_p),
         ("unit_items", ctypes.c_void_p), ("work_items", ctypes.c_void_p), ("counters", ctypes.c_void_p),
-        ("partials", ctypes.c_void_p), ("head_page_bits", ctypes.c_void_p), ("max_items", ctypes.c_int64),
+        ("partials", ctypes.c_void_p), ("head_page_bits", ctypes.c_void_p), ("sel_bits", ctypes.c_void_p),
+        ("unit_done", ctypes.c_void_p), ("band_idx", ctypes.c_void_p), ("band_scores", ctypes.c_void_p),
+        ("max_items", ctypes.c_int64),
     ]
 
 

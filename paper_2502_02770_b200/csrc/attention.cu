@@ -1,333 +1,506 @@
 // K4 sparse / K5 dense paged decode attention.
 //
 // Reference: attention_weights (attention.py:89-103) + sparse_attention with
-// renormalize=True (attention.py:106-136), as run per head over the group's
-// shared final set at pipeline.py:366-375:  out = w[S] @ V[S] / sum(w[S]) with
-// w = softmax(K q / sqrt d) -- i.e. the softmax restricted to S.  Dense decode
-// (K5) is the same over every token (bypass_config, pipeline.py:129-136).
+// renormalize=True (attention.py:106-136), run per head over the group's
+// shared final set at pipeline.py:366-375: out = w[S] @ V[S] / sum(w[S]), w =
+// softmax(K q / sqrt d) -- the softmax restricted to S.  Dense decode (K5) is
+// the same over every token (bypass_config, pipeline.py:129-136).
 //
-// Load balancing: the surviving sets of different units
-// differ by orders of magnitude, so work is flattened into fixed-size
-// (unit, token-chunk) items produced on device by K3c; a persistent grid walks
-// the item list and a merge kernel combines split-KV partial (m, l, o) states.
-// All G query heads of a KV head read each gathered K/V row once.
+// Load balancing: surviving sets differ by orders of
+// magnitude between units, so the work is flattened into fixed-size
+// (unit, token chunk) items built on device by K3c.  Every WARP is an
+// independent worker walking that list; split units are merged afterwards
+// (split-KV log-sum-exp) by a small parallel merge kernel.
 //
-// Mapping: 4 warps per CTA, a half-warp per token row (16 lanes x 8 channels
-// = one coalesced 256-B bf16 row), 8 rows per half-warp per 64-token
-// sub-chunk, all K and V loads of a sub-chunk issued before any math.
+// Per warp: a 3-stage cp.async (LDGSTS, 16 B per lane) ring of 16-row K/V
+// tiles, XOR-swizzled so ldmatrix is bank-conflict free.  (Measured on B200,
+// tools/tma_bench.cu: cp.async.bulk costs ~70 cycles per copy per issuing
+// CTA, i.e. ~1 TB/s for 256-B row gathers at one CTA/SM, while LDGSTS moves
+// 512 B per instruction.)  Both products run on tensor cores (mma.sync bf16):
+//   S^T[rows x heads]  = K[rows x d] . Q^T[d x heads]      (rows in M, G<=8 heads in N)
+//   O^T[d x heads]    += V^T[d x rows] . P^T[rows x heads] (P split into bf16 hi+lo)
+// so every gathered row is read once and used by all G heads at a handful of
+// issued instructions per row.  The fp32 (parity) variant uses CUDA cores.
 #include "common.cuh"
 
 namespace tw {
 
-constexpr int kAttWarps = 4;
-constexpr int kSub = 64;  // tokens per sub-chunk (8 half-warps x 8 rows)
+constexpr int kAttWarps = 4;            // warps (= independent workers) per CTA
+constexpr int kAttThreads = kAttWarps * 32;
+constexpr int kTile = 16;               // rows per stage
+constexpr int kNS = 3;                  // stages per warp
+constexpr int kMaxChunk = 512;          // tokens per work item (upper bound)
+constexpr int kDefaultChunk = TW_DEFAULT_CHUNK;
+constexpr int kDenseChunk = 512;
 
 template <typename T>
-struct RowLoad;  // 8 channels of one row for one lane
-template <>
-struct RowLoad<__nv_bfloat16> {
-  uint4 v;
-  __device__ __forceinline__ void load(const __nv_bfloat16* p) { v = ld_stream(p); }
-  __device__ __forceinline__ void get(float (&o)[8]) const { cvt8(v, (const __nv_bfloat16*)nullptr, o); }
-  __device__ __forceinline__ void zero() { v = make_uint4(0, 0, 0, 0); }
+struct WarpSmem {
+  alignas(128) T k[kNS][kTile][kHeadDim];
+  alignas(128) T v[kNS][kTile][kHeadDim];
+  uint32_t rows[kMaxChunk];  // row index (element offset / 128) of every row of the current item
 };
-template <>
-struct RowLoad<float> {
-  uint4 a, b;
-  __device__ __forceinline__ void load(const float* p) { a = ld_stream(p); b = ld_stream(p + 4); }
-  __device__ __forceinline__ void get(float (&o)[8]) const {
-    o[0] = __uint_as_float(a.x); o[1] = __uint_as_float(a.y); o[2] = __uint_as_float(a.z); o[3] = __uint_as_float(a.w);
-    o[4] = __uint_as_float(b.x); o[5] = __uint_as_float(b.y); o[6] = __uint_as_float(b.z); o[7] = __uint_as_float(b.w);
+
+struct ItemDesc {
+  int unit, start, count, nitems, slot;
+};
+
+template <bool DENSE>
+__device__ __forceinline__ ItemDesc get_item(const tw_paged_kv& kv, const tw_decode_buffers& buf, int it,
+                                             int chunk, int max_chunks) {
+  ItemDesc d;
+  if (DENSE) {
+    d.unit = it / max_chunks;
+    const int c = it % max_chunks;
+    const int n = kv.seq_lens[d.unit / kv.num_kv_heads];
+    d.start = c * chunk;
+    d.count = min(chunk, n - d.start);
+    d.nitems = (n + chunk - 1) / chunk;
+  } else {
+    d.unit = buf.work_items[2 * it];
+    d.start = buf.work_items[2 * it + 1];
+    d.count = min(chunk, buf.final_count[d.unit] - d.start);
+    d.nitems = buf.unit_items[2 * d.unit + 1];
   }
-  __device__ __forceinline__ void zero() { a = b = make_uint4(0, 0, 0, 0); }
+  d.slot = it;
+  return d;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// swizzled byte offset of 16-B chunk c (0..15) of row i inside a bf16 tile
+__device__ __forceinline__ int swz(int i, int c) { return i * 256 + ((c ^ (i & 7)) << 4); }
+
+// Issue the cp.async copies of stage s (rows 16s .. 16s+15 of the item).
+template <typename T>
+__device__ __forceinline__ void issue_stage(WarpSmem<T>& W, const tw_paged_kv& kv, int s, int count, int slot) {
+  const int lane = threadIdx.x & 31;
+  constexpr int kChunks = kHeadDim * sizeof(T) / 16;  // 16 (bf16) or 32 (fp32) per row
+  constexpr int kRowsPerInst = 32 / kChunks;          // 2 or 1
+  const int c = lane % kChunks;
+  char* kd = reinterpret_cast<char*>(&W.k[slot][0][0]);
+  char* vd = reinterpret_cast<char*>(&W.v[slot][0][0]);
+#pragma unroll
+  for (int i0 = 0; i0 < kTile; i0 += kRowsPerInst) {
+    const int i = i0 + lane / kChunks;
+    const int j = s * kTile + i;
+    if (j < count) {
+      const size_t off = (size_t)W.rows[j] * kHeadDim;
+      const char* ks = reinterpret_cast<const char*>(reinterpret_cast<const T*>(kv.k_cache) + off) + 16 * c;
+      const char* vs = reinterpret_cast<const char*>(reinterpret_cast<const T*>(kv.v_cache) + off) + 16 * c;
+      const int o = sizeof(T) == 2 ? swz(i, c) : i * kHeadDim * 4 + 16 * c;
+      cp_async16(kd + o, ks);
+      cp_async16(vd + o, vs);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ bf16 consumer (tensor cores)
+
+struct StateMMA {
+  float m[2], l[2];
+  float o[8][4];  // O^T: m-tile i (channels 16i..16i+15) x heads (2t, 2t+1)
+};
+
+__device__ __forceinline__ void consume_mma(StateMMA& st, const uint32_t (&qb)[8][2], const char* K,
+                                            const char* V, int rows) {
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2, t = lane & 3, q8 = lane >> 3, rr = lane & 7;
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+  {
+    const int row = (q8 & 1) * 8 + rr;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t a[4];
+      ldsm_x4(a, K + swz(row, kk * 2 + (q8 >> 1)));
+      mma16816(s, a, qb[kk][0], qb[kk][1]);
+    }
+  }
+  const float sc = 0.08838834764831845f;  // 1/sqrt(128)
+  s[0] = r < rows ? s[0] * sc : -INFINITY;
+  s[1] = r < rows ? s[1] * sc : -INFINITY;
+  s[2] = r + 8 < rows ? s[2] * sc : -INFINITY;
+  s[3] = r + 8 < rows ? s[3] * sc : -INFINITY;
+  float alpha[2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    float mx = fmaxf(s[c], s[c + 2]);
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    const float mn = fmaxf(st.m[c], mx);
+    alpha[c] = (st.m[c] == -INFINITY) ? 0.f : __expf(st.m[c] - mn);
+    s[c] = (s[c] == -INFINITY) ? 0.f : __expf(s[c] - mn);
+    s[c + 2] = (s[c + 2] == -INFINITY) ? 0.f : __expf(s[c + 2] - mn);
+    float ps = s[c] + s[c + 2];
+    ps += __shfl_xor_sync(0xffffffffu, ps, 4);
+    ps += __shfl_xor_sync(0xffffffffu, ps, 8);
+    ps += __shfl_xor_sync(0xffffffffu, ps, 16);
+    st.l[c] = st.l[c] * alpha[c] + ps;
+    st.m[c] = mn;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    st.o[i][0] *= alpha[0];
+    st.o[i][1] *= alpha[1];
+    st.o[i][2] *= alpha[0];
+    st.o[i][3] *= alpha[1];
+  }
+  // P^T B fragments from the S^T accumulators (rows 2t,2t+1 | 2t+8,2t+9 of head g)
+  const int g = lane >> 2;
+  const int srcA = 8 * t + (g >> 1), srcB = srcA + 4;
+  const uint32_t selp = (g & 1) ? 0x7632u : 0x5410u;
+  const uint32_t h01 = pack_bf16(s[0], s[1]), h23 = pack_bf16(s[2], s[3]);
+  const __nv_bfloat162 hb01 = *reinterpret_cast<const __nv_bfloat162*>(&h01);
+  const __nv_bfloat162 hb23 = *reinterpret_cast<const __nv_bfloat162*>(&h23);
+  const uint32_t l01 = pack_bf16(s[0] - __low2float(hb01), s[1] - __high2float(hb01));
+  const uint32_t l23 = pack_bf16(s[2] - __low2float(hb23), s[3] - __high2float(hb23));
+  const uint32_t bh0 = __byte_perm(__shfl_sync(0xffffffffu, h01, srcA), __shfl_sync(0xffffffffu, h01, srcB), selp);
+  const uint32_t bh1 = __byte_perm(__shfl_sync(0xffffffffu, h23, srcA), __shfl_sync(0xffffffffu, h23, srcB), selp);
+  const uint32_t bl0 = __byte_perm(__shfl_sync(0xffffffffu, l01, srcA), __shfl_sync(0xffffffffu, l01, srcB), selp);
+  const uint32_t bl1 = __byte_perm(__shfl_sync(0xffffffffu, l23, srcA), __shfl_sync(0xffffffffu, l23, srcB), selp);
+  const int vrow = (q8 >> 1) * 8 + rr;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t a[4];
+    ldsm_x4_t(a, V + swz(vrow, 2 * i + (q8 & 1)));
+    mma16816(st.o[i], a, bh0, bh1);
+    mma16816(st.o[i], a, bl0, bl1);
+  }
+}
+
+// ------------------------------------------------------------------ fp32 consumer (CUDA cores)
+
+template <int G>
+struct StateF32 {
+  float m[G], l[G], o[G][4];  // lane owns channels 4*lane .. 4*lane+3
 };
 
 template <int G>
-struct AttnSmem {
-  float s[kSub][G];             // scores of the sub-chunk
-  float m_new[G], alpha[G];
-  float m[G], l[G];
-  float red[2 * kAttWarps][G][kHeadDim];  // cross-half-warp reduction of o
-};
-
-// Attend the query heads of `unit` over `count` tokens given by `ids`
-// (or the contiguous range [t0, t0+count) when ids == nullptr).
-// Leaves the un-normalised o in red[0], and m, l in smem.
-template <typename T, int G>
-__device__ __forceinline__ void attend(const tw_paged_kv& kv, const T* __restrict__ q, int unit,
-                                       const int* __restrict__ ids, int t0, int count, AttnSmem<G>& S) {
-  const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sub = lane & 15, hw = warp * 2 + (lane >> 4);  // half-warp 0..7
-  const int* pt = kv.page_table + (size_t)b * kv.max_pages;
-  const T* kc = reinterpret_cast<const T*>(kv.k_cache);
-  const T* vc = reinterpret_cast<const T*>(kv.v_cache);
-  const float inv_sqrt_d = 0.08838834764831845f;
-
-  float qf[G][8];
+__device__ __forceinline__ void consume_f32(StateF32<G>& st, const float (&qf)[G][4], const float* K,
+                                            const float* V, int rows) {
+  const int lane = threadIdx.x & 31;
+  const float sc = 0.08838834764831845f;
+  for (int i = 0; i < rows; ++i) {
+    const float4 k4 = *reinterpret_cast<const float4*>(K + i * kHeadDim + 4 * lane);
+    const float4 v4 = *reinterpret_cast<const float4*>(V + i * kHeadDim + 4 * lane);
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    load8(q + ((size_t)unit * G + g) * kHeadDim + 8 * sub, qf[g]);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) qf[g][i] *= inv_sqrt_d;
-  }
-  float o[G][8];
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) o[g][i] = 0.f;
-  if (threadIdx.x < G) { S.m[threadIdx.x] = -INFINITY; S.l[threadIdx.x] = 0.f; }
-
-  for (int c0 = 0; c0 < count; c0 += kSub) {
-    RowLoad<T> kr[8], vr[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int j = c0 + hw + 8 * i;
-      if (j < count) {
-        const int tok = ids ? ids[j] : t0 + j;
-        const size_t row = (((size_t)pt[tok >> 4] * kv.num_kv_heads + h) * kPage + (tok & 15)) * kHeadDim + 8 * sub;
-        kr[i].load(kc + row);
-        vr[i].load(vc + row);
-      } else {
-        kr[i].zero();
-        vr[i].zero();
-      }
+    for (int g = 0; g < G; ++g) {
+      float a = qf[g][0] * k4.x + qf[g][1] * k4.y + qf[g][2] * k4.z + qf[g][3] * k4.w;
+      a = warp_sum(a) * sc;
+      const float mn = fmaxf(st.m[g], a);
+      const float al = st.m[g] == -INFINITY ? 0.f : expf(st.m[g] - mn);
+      const float p = expf(a - mn);
+      st.l[g] = st.l[g] * al + p;
+      st.m[g] = mn;
+      st.o[g][0] = fmaf(p, v4.x, st.o[g][0] * al);
+      st.o[g][1] = fmaf(p, v4.y, st.o[g][1] * al);
+      st.o[g][2] = fmaf(p, v4.z, st.o[g][2] * al);
+      st.o[g][3] = fmaf(p, v4.w, st.o[g][3] * al);
     }
-    // scores
+  }
+}
+
+// ------------------------------------------------------------------ the kernel
+
+template <typename T, int G, bool DENSE>
+__global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const T* __restrict__ q,
+                                                           tw_decode_buffers buf, float* __restrict__ out,
+                                                           int chunk, int max_chunks, int total_items) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpSmem<T>& W = reinterpret_cast<WarpSmem<T>*>(smem_raw)[warp];
+  const int nitems_total = DENSE ? total_items : min((int)buf.counters[0], total_items);
+  const size_t T_stride = (size_t)kv.max_pages * kPage;
+  const int H = kv.num_kv_heads;
+  const int gw = blockIdx.x * kAttWarps + warp, nw = gridDim.x * kAttWarps;
+  const int r = lane >> 2, t = lane & 3;
+
+  for (int it = gw; it < nitems_total; it += nw) {
+    const ItemDesc d = get_item<DENSE>(kv, buf, it, chunk, max_chunks);
+    if (d.count <= 0) continue;
+    const int b = d.unit / H, h = d.unit % H;
+    // row indices of the whole item (all index loads in flight together)
+    {
+      const int* pt = kv.page_table + (size_t)b * kv.max_pages;
+      const int* ids = DENSE ? nullptr : buf.final_idx + d.unit * T_stride + d.start;
+      __syncwarp();
+      for (int j = lane; j < d.count; j += 32) {
+        const int tok = DENSE ? d.start + j : __ldg(ids + j);
+        W.rows[j] = ((uint32_t)__ldg(pt + (tok >> 4)) * H + h) * kPage + (tok & 15);
+      }
+      __syncwarp();
+    }
+    const int nst = (d.count + kTile - 1) / kTile;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float kf[8];
-      kr[i].get(kf);
-      float sc[G];
+    for (int s = 0; s < kNS - 1; ++s) {
+      if (s < nst) issue_stage<T>(W, kv, s, d.count, s);
+      cp_commit();
+    }
+    const T* qu = q + (size_t)d.unit * G * kHeadDim;
+    float* part = buf.partials + (size_t)d.slot * G * (kHeadDim + 2);
+    const bool single = d.nitems == 1;
+    if constexpr (sizeof(T) == 2) {
+      uint32_t qb[8][2];
+      const int g = lane >> 2;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if (g < G) {
+          const uint32_t* qw = reinterpret_cast<const uint32_t*>(qu + g * kHeadDim + kk * 16);
+          qb[kk][0] = __ldg(qw + t);
+          qb[kk][1] = __ldg(qw + t + 4);
+        } else {
+          qb[kk][0] = qb[kk][1] = 0u;
+        }
+      }
+      StateMMA st;
+      st.m[0] = st.m[1] = -INFINITY;
+      st.l[0] = st.l[1] = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) st.o[i][0] = st.o[i][1] = st.o[i][2] = st.o[i][3] = 0.f;
+      for (int s = 0; s < nst; ++s) {
+        if (s + kNS - 1 < nst) issue_stage<T>(W, kv, s + kNS - 1, d.count, (s + kNS - 1) % kNS);
+        cp_commit();
+        cp_wait<kNS - 1>();
+        __syncwarp();
+        const int slot = s % kNS;
+        const int rows = min(kTile, d.count - s * kTile);
+        if (rows < kTile) {  // 0 * stale smem would poison the PV product: clear unused V rows
+          uint4* vz = reinterpret_cast<uint4*>(&W.v[slot][rows][0]);
+          for (int z = lane; z < (kTile - rows) * 16; z += 32) vz[z] = make_uint4(0, 0, 0, 0);
+          __syncwarp();
+        }
+        consume_mma(st, qb, reinterpret_cast<const char*>(&W.k[slot][0][0]),
+                    reinterpret_cast<const char*>(&W.v[slot][0][0]), rows);
+        __syncwarp();
+      }
+      // emit: lane holds heads 2t, 2t+1 for channels 16i + r (+8)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int g2 = 2 * t + c;
+        if (g2 < G) {
+          const float inv = st.l[c] > 0.f ? 1.f / st.l[c] : 0.f;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int c0 = 16 * i + r;
+            if (single) {
+              out[((size_t)d.unit * G + g2) * kHeadDim + c0] = st.o[i][c] * inv;
+              out[((size_t)d.unit * G + g2) * kHeadDim + c0 + 8] = st.o[i][c + 2] * inv;
+            } else {
+              part[g2 * (kHeadDim + 2) + c0] = st.o[i][c];
+              part[g2 * (kHeadDim + 2) + c0 + 8] = st.o[i][c + 2];
+            }
+          }
+          if (!single && r == 0) {
+            part[g2 * (kHeadDim + 2) + kHeadDim] = st.m[c];
+            part[g2 * (kHeadDim + 2) + kHeadDim + 1] = st.l[c];
+          }
+        }
+      }
+    } else {
+      float qf[G][4];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        float a = 0.f;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) a = fmaf(qf[g][e], kf[e], a);
-        sc[g] = a;
+        const float4 v = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(qu) + g * kHeadDim + 4 * lane);
+        qf[g][0] = v.x; qf[g][1] = v.y; qf[g][2] = v.z; qf[g][3] = v.w;
       }
+      StateF32<G> st;
 #pragma unroll
-      for (int off = 8; off > 0; off >>= 1)
-#pragma unroll
-        for (int g = 0; g < G; ++g) sc[g] += __shfl_xor_sync(0xffffffffu, sc[g], off);
-      const int j = hw + 8 * i;
-      if (sub == 0) {
-#pragma unroll
-        for (int g = 0; g < G; ++g) S.s[j][g] = (c0 + j < count) ? sc[g] : -INFINITY;
+      for (int g = 0; g < G; ++g) {
+        st.m[g] = -INFINITY;
+        st.l[g] = 0.f;
+        st.o[g][0] = st.o[g][1] = st.o[g][2] = st.o[g][3] = 0.f;
       }
-    }
-    __syncthreads();
-    // per-head max of the sub-chunk and rescale factor
-    if (warp < G || (G > kAttWarps)) {
-      for (int g = warp; g < G; g += kAttWarps) {
-        float mx = fmaxf(S.s[lane][g], S.s[lane + 32][g]);
-        mx = warp_max(mx);
-        const float mo = S.m[g];
-        const float mn = fmaxf(mo, mx);
-        const float e0 = mn == -INFINITY ? 0.f : __expf(S.s[lane][g] - mn);
-        const float e1 = mn == -INFINITY ? 0.f : __expf(S.s[lane + 32][g] - mn);
-        const float ls = warp_sum(e0 + e1);
+      for (int s = 0; s < nst; ++s) {
+        if (s + kNS - 1 < nst) issue_stage<T>(W, kv, s + kNS - 1, d.count, (s + kNS - 1) % kNS);
+        cp_commit();
+        cp_wait<kNS - 1>();
         __syncwarp();
-        S.s[lane][g] = e0;
-        S.s[lane + 32][g] = e1;
-        if (lane == 0) {
-          const float al = (mo == -INFINITY) ? 0.f : __expf(mo - mn);
-          S.alpha[g] = al;
-          S.m[g] = mn;
-          S.l[g] = S.l[g] * al + ls;
+        const int slot = s % kNS;
+        consume_f32<G>(st, qf, reinterpret_cast<const float*>(&W.k[slot][0][0]),
+                       reinterpret_cast<const float*>(&W.v[slot][0][0]), min(kTile, d.count - s * kTile));
+        __syncwarp();
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float inv = st.l[g] > 0.f ? 1.f / st.l[g] : 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (single)
+            out[((size_t)d.unit * G + g) * kHeadDim + 4 * lane + e] = st.o[g][e] * inv;
+          else
+            part[g * (kHeadDim + 2) + 4 * lane + e] = st.o[g][e];
+        }
+        if (!single && lane == 0) {
+          part[g * (kHeadDim + 2) + kHeadDim] = st.m[g];
+          part[g * (kHeadDim + 2) + kHeadDim + 1] = st.l[g];
         }
       }
     }
-    __syncthreads();
-    // o = o * alpha + sum p v
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float al = S.alpha[g];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) o[g][e] *= al;
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float vf[8];
-      vr[i].get(vf);
-      const int j = hw + 8 * i;
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float pj = S.s[j][g];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[g][e] = fmaf(pj, vf[e], o[g][e]);
-      }
-    }
-    __syncthreads();
+    cp_wait<0>();
   }
-  // reduce o over the 8 half-warps
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) S.red[hw][g][8 * sub + e] = o[g][e];
-  __syncthreads();
-  for (int x = threadIdx.x; x < G * kHeadDim; x += blockDim.x) {
-    const int g = x / kHeadDim, c = x % kHeadDim;
-    float s = 0.f;
-#pragma unroll
-    for (int k = 0; k < 2 * kAttWarps; ++k) s += S.red[k][g][c];
-    S.red[0][g][c] = s;
-  }
-  __syncthreads();
-}
-
-// write either the final normalised output or a split-KV partial
-template <int G>
-__device__ __forceinline__ void emit(AttnSmem<G>& S, int unit, bool single, float* out, float* partial) {
-  for (int x = threadIdx.x; x < G * kHeadDim; x += blockDim.x) {
-    const int g = x / kHeadDim, c = x % kHeadDim;
-    const float o = S.red[0][g][c];
-    if (single) {
-      const float l = S.l[g];
-      out[((size_t)unit * G + g) * kHeadDim + c] = l > 0.f ? o / l : 0.f;
-    } else {
-      partial[(size_t)g * (kHeadDim + 2) + c] = o;
-      if (c == 0) {
-        partial[(size_t)g * (kHeadDim + 2) + kHeadDim] = S.m[g];
-        partial[(size_t)g * (kHeadDim + 2) + kHeadDim + 1] = S.l[g];
-      }
-    }
+  // units whose final set is empty: zeros (sparse_attention, attention.py:126-129)
+  if (!DENSE) {
+    const int units = kv.num_seqs * H;
+    for (int u = gw; u < units; u += nw)
+      if (buf.final_count[u] == 0)
+        for (int x = lane; x < G * kHeadDim; x += 32) out[(size_t)u * G * kHeadDim + x] = 0.f;
   }
 }
 
-// K4: persistent walk over the device-built work list
-template <typename T, int G>
-__global__ void __launch_bounds__(kAttWarps * 32) sparse_attn_kernel(tw_paged_kv kv, const T* __restrict__ q,
-                                                                     tw_decode_params prm, tw_decode_buffers buf,
-                                                                     float* __restrict__ out) {
-  __shared__ AttnSmem<G> S;
-  const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : 64;
-  const int nitems = min((int)buf.counters[0], (int)buf.max_items);
-  const size_t T_stride = (size_t)kv.max_pages * kPage;
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const int unit = buf.work_items[2 * it];
-    const int start = buf.work_items[2 * it + 1];
-    const int cnt = min(chunk, buf.final_count[unit] - start);
-    attend<T, G>(kv, q, unit, buf.final_idx + unit * T_stride + start, 0, cnt, S);
-    const bool single = buf.unit_items[2 * unit + 1] == 1;
-    emit<G>(S, unit, single, out, buf.partials + (size_t)it * G * (kHeadDim + 2));
-    __syncthreads();
-  }
-  // units whose final set is empty: zeros (sparse_attention without renormalisation, attention.py:126-129)
-  const int units = kv.num_seqs * kv.num_kv_heads;
-  for (int u = blockIdx.x; u < units; u += gridDim.x)
-    if (buf.final_count[u] == 0)
-      for (int x = threadIdx.x; x < G * kHeadDim; x += blockDim.x) out[(size_t)u * G * kHeadDim + x] = 0.f;
-}
-
-// merge split-KV partials: one CTA per unit, thread per (head, channel)
-template <int G>
-__global__ void merge_kernel(const tw_paged_kv kv, const int32_t* __restrict__ unit_items,
-                             const float* __restrict__ partials, float* __restrict__ out, int dense_chunks,
-                             int dense_chunk) {
+// Merge the split-KV partials of every unit with more than one item:
+// one CTA per unit; weights exp(m_i - M) first, then coalesced weighted sums.
+template <int G, bool DENSE>
+__global__ void __launch_bounds__(256) merge_kernel(tw_paged_kv kv, tw_decode_buffers buf, float* __restrict__ out,
+                                                    int chunk, int max_chunks) {
+  __shared__ float w[2048];
+  __shared__ float Lsum[8];
   const int unit = blockIdx.x;
   int first, n;
-  if (dense_chunks > 0) {
-    first = unit * dense_chunks;
-    n = (kv.seq_lens[unit / kv.num_kv_heads] + dense_chunk - 1) / dense_chunk;
+  if (DENSE) {
+    const int len = kv.seq_lens[unit / kv.num_kv_heads];
+    first = unit * max_chunks;
+    n = (len + chunk - 1) / chunk;
   } else {
-    first = unit_items[2 * unit];
-    n = unit_items[2 * unit + 1];
+    first = buf.unit_items[2 * unit];
+    n = buf.unit_items[2 * unit + 1];
   }
-  if (n <= 1 && dense_chunks == 0) return;
+  if (n <= 1) return;
+  const float* P = buf.partials;
+  for (int x = threadIdx.x; x < G * n; x += blockDim.x) {
+    const int g = x / n, i = x % n;
+    w[x] = P[((size_t)(first + i) * G + g) * (kHeadDim + 2) + kHeadDim];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int g = warp; g < G; g += blockDim.x / 32) {
+    float M = -INFINITY;
+    for (int i = lane; i < n; i += 32) M = fmaxf(M, w[g * n + i]);
+    M = warp_max(M);
+    float L = 0.f;
+    for (int i = lane; i < n; i += 32) {
+      const float mi = w[g * n + i];
+      const float e = mi == -INFINITY ? 0.f : __expf(mi - M);
+      L += e * P[((size_t)(first + i) * G + g) * (kHeadDim + 2) + kHeadDim + 1];
+      w[g * n + i] = e;
+    }
+    L = warp_sum(L);
+    if (lane == 0) Lsum[g] = L;
+  }
+  __syncthreads();
   for (int x = threadIdx.x; x < G * kHeadDim; x += blockDim.x) {
     const int g = x / kHeadDim, c = x % kHeadDim;
-    float M = -INFINITY;
-    for (int i = 0; i < n; ++i) M = fmaxf(M, partials[((size_t)(first + i) * G + g) * (kHeadDim + 2) + kHeadDim]);
-    float L = 0.f, o = 0.f;
-    for (int i = 0; i < n; ++i) {
-      const float* pp = partials + ((size_t)(first + i) * G + g) * (kHeadDim + 2);
-      const float mi = pp[kHeadDim];
-      if (mi == -INFINITY) continue;
-      const float sc = __expf(mi - M);
-      L += pp[kHeadDim + 1] * sc;
-      o += pp[c] * sc;
+    float O = 0.f;
+    int i = 0;
+    for (; i + 8 <= n; i += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = P[((size_t)(first + i + u) * G + g) * (kHeadDim + 2) + c];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) O = fmaf(w[g * n + i + u], v[u], O);
     }
-    out[((size_t)unit * G + g) * kHeadDim + c] = L > 0.f ? o / L : 0.f;
+    for (; i < n; ++i) O = fmaf(w[g * n + i], P[((size_t)(first + i) * G + g) * (kHeadDim + 2) + c], O);
+    const float L = Lsum[g];
+    out[((size_t)unit * G + g) * kHeadDim + c] = L > 0.f ? O / L : 0.f;
   }
-}
-
-// K5: grid (chunks, units); every chunk writes a partial, merged afterwards
-template <typename T, int G>
-__global__ void __launch_bounds__(kAttWarps * 32) dense_attn_kernel(tw_paged_kv kv, const T* __restrict__ q,
-                                                                    float* __restrict__ partials, int chunk) {
-  __shared__ AttnSmem<G> S;
-  const int unit = blockIdx.y;
-  const int n = kv.seq_lens[unit / kv.num_kv_heads];
-  const int t0 = blockIdx.x * chunk;
-  if (t0 >= n) return;
-  attend<T, G>(kv, q, unit, nullptr, t0, min(chunk, n - t0), S);
-  emit<G>(S, unit, false, nullptr, partials + ((size_t)unit * gridDim.x + blockIdx.x) * G * (kHeadDim + 2));
 }
 
 }  // namespace tw
 
 using namespace tw;
 
-constexpr int kDenseChunk = 512;
-
-template <typename T, int G>
-static int launch_sparse(const tw_paged_kv* kv, const T* q, const tw_decode_params* prm,
-                         const tw_decode_buffers* buf, float* out, cudaStream_t s) {
+template <typename T, int G, bool DENSE>
+static int launch_attn(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, float* out, int chunk,
+                       cudaStream_t s) {
   const int units = kv->num_seqs * kv->num_kv_heads;
+  const int T_tokens = kv->max_pages * kPage;
+  const int max_chunks = (T_tokens + chunk - 1) / chunk;
+  const int total = DENSE ? units * max_chunks : (int)buf->max_items;
+  if (chunk > kMaxChunk || chunk % kTile != 0) return TW_ERR_INVALID;
+  if ((int64_t)max_chunks * G > 2048) return TW_ERR_INVALID;  // merge weights fit shared memory
+  if (DENSE && (int64_t)units * max_chunks > buf->max_items) return TW_ERR_INVALID;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = sms * 8;
-  sparse_attn_kernel<T, G><<<grid, kAttWarps * 32, 0, s>>>(*kv, q, *prm, *buf, out);
-  merge_kernel<G><<<units, 256, 0, s>>>(*kv, buf->unit_items, buf->partials, out, 0, 0);
+  const size_t smem = sizeof(WarpSmem<T>) * kAttWarps;
+  auto kern = attn_kernel<T, G, DENSE>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAttThreads, smem);
+  per_sm = per_sm < 1 ? 1 : per_sm;
+  int grid = sms * per_sm;
+  if (DENSE && grid * kAttWarps > total) grid = (total + kAttWarps - 1) / kAttWarps;
+  kern<<<grid, kAttThreads, smem, s>>>(*kv, q, *buf, out, chunk, max_chunks, total);
+  merge_kernel<G, DENSE><<<units, 256, 0, s>>>(*kv, *buf, out, chunk, max_chunks);
   return launch_status();
 }
 
-template <typename T, int G>
-static int launch_dense(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, float* out,
-                        cudaStream_t s) {
-  const int units = kv->num_seqs * kv->num_kv_heads;
-  const int chunks = (kv->max_pages * kPage + kDenseChunk - 1) / kDenseChunk;
-  if ((int64_t)chunks * units > buf->max_items) return TW_ERR_INVALID;
-  dense_attn_kernel<T, G><<<dim3(chunks, units), kAttWarps * 32, 0, s>>>(*kv, q, buf->partials, kDenseChunk);
-  merge_kernel<G><<<units, 256, 0, s>>>(*kv, nullptr, buf->partials, out, chunks, kDenseChunk);
-  return launch_status();
-}
-
-#define TW_DISPATCH_G(G_, CALL) \
-  switch (G_) {                 \
+#define TW_DISPATCH_G(G_, CALL)                    \
+  switch (G_) {                                    \
     case 1: { constexpr int GG = 1; return CALL; } \
     case 2: { constexpr int GG = 2; return CALL; } \
     case 4: { constexpr int GG = 4; return CALL; } \
     case 8: { constexpr int GG = 8; return CALL; } \
-    default: return TW_ERR_INVALID; \
+    default: return TW_ERR_INVALID;                \
   }
+
+static inline int sparse_chunk(const tw_decode_params* prm) {
+  return prm->chunk_tokens > 0 ? prm->chunk_tokens : kDefaultChunk;
+}
 
 extern "C" int tw_sparse_attention(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
                                    const tw_decode_buffers* buf, float* out, cudaStream_t stream) {
   if (!kv || !q || !prm || !buf || !out || kv->head_dim != kHeadDim || !buf->partials) return TW_ERR_INVALID;
   if (prm->renormalize != 1) return TW_ERR_INVALID;
+  const int chunk = sparse_chunk(prm);
   if (kv->dtype == TW_BF16) {
-    TW_DISPATCH_G(kv->group_size, (launch_sparse<__nv_bfloat16, GG>(kv, (const __nv_bfloat16*)q, prm, buf, out, stream)))
+    TW_DISPATCH_G(kv->group_size,
+                  (launch_attn<__nv_bfloat16, GG, false>(kv, (const __nv_bfloat16*)q, buf, out, chunk, stream)))
   }
-  TW_DISPATCH_G(kv->group_size, (launch_sparse<float, GG>(kv, (const float*)q, prm, buf, out, stream)))
+  TW_DISPATCH_G(kv->group_size, (launch_attn<float, GG, false>(kv, (const float*)q, buf, out, chunk, stream)))
 }
 
 extern "C" int tw_dense_attention(const tw_paged_kv* kv, const void* q, const tw_decode_buffers* buf, float* out,
                                   cudaStream_t stream) {
   if (!kv || !q || !buf || !out || kv->head_dim != kHeadDim || !buf->partials) return TW_ERR_INVALID;
   if (kv->dtype == TW_BF16) {
-    TW_DISPATCH_G(kv->group_size, (launch_dense<__nv_bfloat16, GG>(kv, (const __nv_bfloat16*)q, buf, out, stream)))
+    TW_DISPATCH_G(kv->group_size,
+                  (launch_attn<__nv_bfloat16, GG, true>(kv, (const __nv_bfloat16*)q, buf, out, kDenseChunk, stream)))
   }
-  TW_DISPATCH_G(kv->group_size, (launch_dense<float, GG>(kv, (const float*)q, buf, out, stream)))
+  TW_DISPATCH_G(kv->group_size, (launch_attn<float, GG, true>(kv, (const float*)q, buf, out, kDenseChunk, stream)))
 }
 
 extern "C" int64_t tw_max_work_items(const tw_paged_kv* kv, int32_t chunk_tokens) {
   if (!kv) return 0;
   const int64_t units = (int64_t)kv->num_seqs * kv->num_kv_heads;
   const int64_t T = (int64_t)kv->max_pages * kPage;
-  const int64_t c = chunk_tokens > 0 ? chunk_tokens : 64;
+  const int64_t c = chunk_tokens > 0 ? chunk_tokens : kDefaultChunk;
   const int64_t sparse = units * ((T + c - 1) / c);
   const int64_t dense = units * ((T + kDenseChunk - 1) / kDenseChunk);
   return sparse > dense ? sparse : dense;

@@ -1,14 +1,29 @@
-// Small block-wide primitives (scan, reductions, radix select) shared by the
-// selection and pruning kernels.
+// Block- and warp-group-wide primitives (scan, reductions, radix select)
+// shared by the selection and pruning kernels.  A Group is a run of whole
+// warps synchronised by a named barrier, so several independent selections
+// can proceed inside one CTA (e.g. the G query heads of a KV head).
 #pragma once
 #include "common.cuh"
 
 namespace tw {
 
-// Inclusive block scan of one u32 per thread; returns the inclusive prefix and
-// writes the block total.  `tmp` must hold blockDim/32 + 1 words.
-__device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t* tmp, uint32_t& total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+struct Group {
+  int bar;       // named barrier id; 0 = __syncthreads (whole block)
+  int nthreads;  // threads in the group (multiple of 32)
+  int tid;       // thread index inside the group
+  __device__ __forceinline__ void sync() const {
+    if (bar == 0) __syncthreads();
+    else named_bar_sync(bar, nthreads);
+  }
+  __device__ __forceinline__ int warp() const { return tid >> 5; }
+  __device__ __forceinline__ int nwarps() const { return nthreads >> 5; }
+};
+
+__device__ __forceinline__ Group whole_block() { return Group{0, (int)blockDim.x, (int)threadIdx.x}; }
+
+// Inclusive scan of one u32 per thread; `tmp` needs nwarps words.
+__device__ __forceinline__ uint32_t group_incl_scan(const Group& g, uint32_t v, uint32_t* tmp, uint32_t& total) {
+  const int lane = g.tid & 31, wid = g.warp(), nw = g.nwarps();
   uint32_t x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -16,21 +31,20 @@ __device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t* tmp, u
     if (lane >= o) x += y;
   }
   if (lane == 31) tmp[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    uint32_t s = lane < nw ? tmp[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
-    }
-    if (lane < nw) tmp[lane] = s;
+  g.sync();
+  uint32_t pre = 0, tot = 0;
+  for (int i = 0; i < nw; ++i) {
+    const uint32_t s = tmp[i];
+    pre += i < wid ? s : 0u;
+    tot += s;
   }
-  __syncthreads();
-  if (wid > 0) x += tmp[wid - 1];
-  total = tmp[nw - 1];
-  __syncthreads();
-  return x;
+  g.sync();
+  total = tot;
+  return x + pre;
+}
+
+__device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t* tmp, uint32_t& total) {
+  return group_incl_scan(whole_block(), v, tmp, total);
 }
 
 template <typename T>
@@ -45,72 +59,88 @@ __device__ __forceinline__ T block_sum(T v, T* tmp) {
   return r;
 }
 
-__device__ __forceinline__ uint32_t block_max_u32(uint32_t v, uint32_t* tmp) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  v = warp_max_u32(v);
-  if (lane == 0) tmp[wid] = v;
-  __syncthreads();
-  uint32_t r = 0;
-  for (int i = 0; i < nw; ++i) r = max(r, tmp[i]);
-  __syncthreads();
-  return r;
+__device__ __forceinline__ void group_minmax_u32(const Group& g, uint32_t& mn, uint32_t& mx, uint32_t* tmp) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((g.tid & 31) == 0) {
+    tmp[2 * g.warp()] = mn;
+    tmp[2 * g.warp() + 1] = mx;
+  }
+  g.sync();
+  for (int i = 0; i < g.nwarps(); ++i) {
+    mn = min(mn, tmp[2 * i]);
+    mx = max(mx, tmp[2 * i + 1]);
+  }
+  g.sync();
 }
 
-// Given per-bin counts hist[0..nbins) (nbins a multiple of blockDim.x),
-// find the bin d* scanning from the TOP bin down such that
+// Given per-bin counts hist[0..nbins) (nbins a multiple of the group size),
+// find bin d* scanning from the TOP bin down with
 //   above = sum_{d > d*} hist[d] < need <= above + hist[d*].
-// Returns d* and writes `above` (uniform across the block).
-__device__ __forceinline__ int block_find_from_top(const uint32_t* hist, int nbins, uint32_t need, uint32_t* tmp,
-                                                   uint32_t& above_out) {
-  const int per = nbins / blockDim.x;
-  // thread t owns bins in descending order: [nbins - (t+1)*per, nbins - t*per)
-  const int hi_bin = nbins - threadIdx.x * per - 1;
+// `res` (2 words of shared memory per group) receives {d*, above}.
+__device__ __forceinline__ int group_find_from_top(const Group& g, const uint32_t* hist, int nbins, uint32_t need,
+                                                   uint32_t* tmp, int* res, uint32_t& above_out) {
+  const int per = nbins / g.nthreads;
+  const int hi_bin = nbins - g.tid * per - 1;
   uint32_t local = 0;
   for (int i = 0; i < per; ++i) local += hist[hi_bin - i];
   uint32_t total;
-  uint32_t incl = block_incl_scan(local, tmp, total);
-  uint32_t excl = incl - local;
-  __shared__ int s_bin;
-  __shared__ uint32_t s_above;
-  if (threadIdx.x == 0) { s_bin = -1; s_above = 0; }
-  __syncthreads();
+  const uint32_t incl = group_incl_scan(g, local, tmp, total);
+  const uint32_t excl = incl - local;
+  if (g.tid == 0) { res[0] = -1; res[1] = 0; }
+  g.sync();
   if (excl < need && need <= incl) {
     uint32_t run = excl;
     for (int i = 0; i < per; ++i) {
-      uint32_t c = hist[hi_bin - i];
-      if (run + c >= need) { s_bin = hi_bin - i; s_above = run; break; }
+      const uint32_t c = hist[hi_bin - i];
+      if (run + c >= need) { res[0] = hi_bin - i; res[1] = (int)run; break; }
       run += c;
     }
   }
-  __syncthreads();
-  int b = s_bin;
-  above_out = s_above;
-  __syncthreads();
+  g.sync();
+  const int b = res[0];
+  above_out = (uint32_t)res[1];
+  g.sync();
   return b;
 }
 
-// K-th largest (1-based k) of n u32 keys held in shared memory.
-// Three radix passes (11, 11, 10 bits); `hist` needs 2048 words.
-__device__ __forceinline__ uint32_t block_kth_largest(const uint32_t* keys, int n, uint32_t k, uint32_t* hist,
-                                                      uint32_t* tmp) {
-  uint32_t prefix = 0, mask = 0, need = k;
-  const int shifts[3] = {21, 10, 0};
-  const int widths[3] = {11, 11, 10};
-#pragma unroll 1
-  for (int pass = 0; pass < 3; ++pass) {
-    const int sh = shifts[pass], nb = 1 << widths[pass];
-    for (int i = threadIdx.x; i < 2048; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      uint32_t kk = keys[i];
-      if ((kk & mask) == prefix) atomicAdd(&hist[(kk >> sh) & (nb - 1)], 1u);
+// k-th largest (1-based) of n u32 keys in shared memory.  Only the bits below
+// the highest bit where the keys differ are radix-scanned (11 bits a pass), so
+// clustered keys (e.g. fp32 scores of similar magnitude) need two passes.
+// `hist` needs 2048 words, `tmp` 2*nwarps words, `res` 2 words.
+__device__ __forceinline__ uint32_t group_kth_largest(const Group& g, const uint32_t* keys, int n, uint32_t k,
+                                                      uint32_t* hist, uint32_t* tmp, int* res) {
+  uint32_t mn = 0xFFFFFFFFu, mx = 0;
+  for (int i = g.tid; i < n; i += g.nthreads) {
+    mn = min(mn, keys[i]);
+    mx = max(mx, keys[i]);
+  }
+  group_minmax_u32(g, mn, mx, tmp);
+  if (mn == mx) return mn;
+  int hi = 31 - __clz(mn ^ mx);
+  uint32_t mask = hi == 31 ? 0u : ~((2u << hi) - 1u);
+  uint32_t prefix = mn & mask;
+  uint32_t need = k;
+  while (hi >= 0) {
+    const int width = hi + 1 < 11 ? hi + 1 : 11;
+    const int sh = hi + 1 - width;
+    const uint32_t dm = (1u << width) - 1u;
+    for (int i = g.tid; i < 2048; i += g.nthreads) hist[i] = 0;
+    g.sync();
+    for (int i = g.tid; i < n; i += g.nthreads) {
+      const uint32_t kk = keys[i];
+      if ((kk & mask) == prefix) atomicAdd(&hist[(kk >> sh) & dm], 1u);
     }
-    __syncthreads();
+    g.sync();
     uint32_t above;
-    int d = block_find_from_top(hist, 2048, need, tmp, above);  // bins >= nb are zero
+    const int d = group_find_from_top(g, hist, 2048, need, tmp, res, above);
     need -= above;
     prefix |= (uint32_t)d << sh;
-    mask |= (uint32_t)(nb - 1) << sh;
+    mask |= dm << sh;
+    hi = sh - 1;
   }
   return prefix;
 }

@@ -111,48 +111,38 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
   const int* cand = buf.cand_pages + (size_t)unit * kv.max_pages;
   const int* pt = kv.page_table + (size_t)b * kv.max_pages;
   const int cend = min(c0 + kEstPagesPerCta, ncand);
-  // page indices of this warp's pages: ci = c0 + warp + 4*i
-  int my_lp = -1, my_phys = 0;
+  // all pages of this warp (ci = c0 + warp + 4*i, i < 8) are loaded up front:
+  // 16 x 16 B of codes + 8 params per lane in flight before the first MMA
+  constexpr int kPPW = kEstPagesPerCta / kEstWarps;
+  int lp_all = 0;
   {
-    const int ci = c0 + warp + 4 * lane;
-    if (lane < 8 && ci < cend) {
-      my_lp = cand[ci];
-      my_phys = pt[my_lp];
+    const int ci = c0 + warp + kEstWarps * lane;
+    if (lane < kPPW && ci < cend) lp_all = cand[ci];
+  }
+  uint4 lo4[kPPW], hi4[kPPW];
+  float prmv[kPPW];
+#pragma unroll
+  for (int i = 0; i < kPPW; ++i) {
+    const int ci = c0 + warp + kEstWarps * i;
+    const int lpi = __shfl_sync(0xffffffffu, lp_all, i);
+    if (ci < cend) {
+      const uint8_t* qb = kv.kq + ((size_t)pt[lpi] * kv.num_kv_heads + h) * kQBlockBytes;
+      lo4[i] = ld_stream(qb + r * 64 + t * 16);
+      hi4[i] = ld_stream(qb + (r + 8) * 64 + t * 16);
+      prmv[i] = __ldg(reinterpret_cast<const float*>(qb + kCodeBytes) + lane);
     }
   }
-  const size_t qstride = kQBlockBytes;
-  auto block_ptr = [&](int phys) {
-    return kv.kq + ((size_t)phys * kv.num_kv_heads + h) * qstride;
-  };
-  int ci = c0 + warp;
-  int it = 0;
-  uint4 lo4 = make_uint4(0, 0, 0, 0), hi4 = lo4;
-  float prmv = 0.f;
-  if (ci < cend) {
-    const uint8_t* qb = block_ptr(__shfl_sync(0xffffffffu, my_phys, 0));
-    lo4 = ld_stream(qb + r * 64 + t * 16);
-    hi4 = ld_stream(qb + (r + 8) * 64 + t * 16);
-    prmv = __ldg(reinterpret_cast<const float*>(qb + kCodeBytes) + lane);
-  }
-  while (ci < cend) {
-    const int lp = __shfl_sync(0xffffffffu, my_lp, it);
-    // prefetch the next page of this warp
-    const int ci_next = ci + kEstWarps;
-    uint4 nlo = make_uint4(0, 0, 0, 0), nhi = nlo;
-    float nprm = 0.f;
-    const int phys_next = __shfl_sync(0xffffffffu, my_phys, (it + 1) & 31);
-    if (ci_next < cend) {
-      const uint8_t* qb = block_ptr(phys_next);
-      nlo = ld_stream(qb + r * 64 + t * 16);
-      nhi = ld_stream(qb + (r + 8) * 64 + t * 16);
-      nprm = __ldg(reinterpret_cast<const float*>(qb + kCodeBytes) + lane);
-    }
+#pragma unroll
+  for (int i = 0; i < kPPW; ++i) {
+    const int ci = c0 + warp + kEstWarps * i;
+    if (ci >= cend) break;
+    const int lp = __shfl_sync(0xffffffffu, lp_all, i);
     // ---- MMA over the 8 k-steps
     float acc[TERMS][4];
 #pragma unroll
     for (int j = 0; j < TERMS; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-    const uint32_t wl[4] = {lo4.x, lo4.y, lo4.z, lo4.w};
-    const uint32_t wh[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
+    const uint32_t wl[4] = {lo4[i].x, lo4[i].y, lo4[i].z, lo4[i].w};
+    const uint32_t wh[4] = {hi4[i].x, hi4[i].y, hi4[i].z, hi4[i].w};
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
       const int m = s >> 1, sh = (s & 1) ? 8 : 0;
@@ -165,8 +155,9 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       for (int j = 0; j < TERMS; ++j) mma_bf16(acc[j], a, bf[j][s][0], bf[j][s][1]);
     }
     // ---- epilogue: rows r and r+8, heads 2t and 2t+1
-    const float sc_r = __shfl_sync(0xffffffffu, prmv, r), sc_r8 = __shfl_sync(0xffffffffu, prmv, r + 8);
-    const float z_r = __shfl_sync(0xffffffffu, prmv, 16 + r), z_r8 = __shfl_sync(0xffffffffu, prmv, 24 + r);
+    const float pv = prmv[i];
+    const float sc_r = __shfl_sync(0xffffffffu, pv, r), sc_r8 = __shfl_sync(0xffffffffu, pv, r + 8);
+    const float z_r = __shfl_sync(0xffffffffu, pv, 16 + r), z_r8 = __shfl_sync(0xffffffffu, pv, 24 + r);
     float d[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -191,11 +182,6 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
         }
       }
     }
-    lo4 = nlo;
-    hi4 = nhi;
-    prmv = nprm;
-    ci = ci_next;
-    ++it;
   }
   // per-head max over this warp -> global (ordered-key atomicMax)
 #pragma unroll

@@ -20,8 +20,6 @@
 namespace tw {
 
 constexpr int kSelThreads = 512;
-constexpr int kAmbMax = 8192;   // ambiguous pages ranked in shared memory per head
-__host__ __device__ inline int amb_cap(int Pmax) { return Pmax < kAmbMax ? Pmax : kAmbMax; }
 constexpr int kFilterPagesPerCta = 64;
 
 // ---------------------------------------------------------------- filter pass
@@ -42,25 +40,35 @@ __global__ void __launch_bounds__(256) quest_filter_kernel(tw_paged_kv kv, const
   for (int g = 0; g < G; ++g) load8(q + ((size_t)unit * G + g) * kHeadDim + 8 * sub, qr[g]);
   const int pend = min(p0 + kFilterPagesPerCta, npages);
   const int* pt = kv.page_table + (size_t)b * kv.max_pages;
-  for (int lp = p0 + warp * 2 + half; lp < pend; lp += 16) {
-    const int phys = pt[lp];
-    const T* lo = reinterpret_cast<const T*>(kv.kmeta) + ((size_t)phys * kv.num_kv_heads + h) * 2 * kHeadDim + 8 * sub;
-    float l8[8], h8[8];
-    load8(lo, l8);
-    load8(lo + kHeadDim, h8);
+  // 4 pages per half-warp, all loads issued before any math
+  constexpr int kU = kFilterPagesPerCta / 16;
+  float l8[kU][8], h8[kU][8];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int lp = p0 + warp * 2 + half + 16 * u;
+    if (lp < pend) {
+      const int phys = pt[lp];
+      const T* lo = reinterpret_cast<const T*>(kv.kmeta) + ((size_t)phys * kv.num_kv_heads + h) * 2 * kHeadDim + 8 * sub;
+      load8(lo, l8[u]);
+      load8(lo + kHeadDim, h8[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int lp = p0 + warp * 2 + half + 16 * u;
     float acc[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       float a = 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a = fmaf(qr[g][i], qr[g][i] >= 0.f ? h8[i] : l8[i], a);
+      for (int i = 0; i < 8; ++i) a = fmaf(qr[g][i], qr[g][i] >= 0.f ? h8[u][i] : l8[u][i], a);
       acc[g] = a;
     }
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1)
 #pragma unroll
       for (int g = 0; g < G; ++g) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
-    if (sub < G) {
+    if (sub < G && lp < pend) {
       float v = acc[0];
 #pragma unroll
       for (int g = 1; g < G; ++g) if (sub == g) v = acc[g];
@@ -123,11 +131,25 @@ __global__ void __launch_bounds__(256) quest_exact_kernel(tw_paged_kv kv, const 
 
 // ---------------------------------------------------------------- select + union
 
-// One CTA per unit (b, kv head); heads processed in turn.
+constexpr int kSelGroups = 4;                       // warp groups: query heads selected concurrently
+constexpr int kGroupThreads = kSelThreads / kSelGroups;
+
+struct SelGroupSmem {
+  uint32_t tmp[2 * (kGroupThreads / 32)];
+  int res[2];
+  int namb, cin;
+  float margin;
+};
+
+// One CTA per unit (b, kv head); its G query heads are spread over 4 warp
+// groups (named barriers 1..4), each running filter-threshold -> band
+// rescoring -> rank on its own head; the CTA then compacts the union.
 template <typename T>
 __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv kv, const T* __restrict__ q,
                                                                    tw_decode_params prm, tw_decode_buffers buf) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ SelGroupSmem GS[kSelGroups];
+  __shared__ uint32_t btmp[kSelThreads / 32];
   const int unit = blockIdx.x;
   const int G = kv.group_size;
   const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
@@ -135,19 +157,17 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
   const int P = (n + kPage - 1) / kPage;
   const int Pmax = kv.max_pages;
   const int words = (Pmax + 31) / 32;
-  uint32_t* keys = reinterpret_cast<uint32_t*>(smem);                 // [Pmax]
-  uint32_t* hist = keys + Pmax;                                        // [2048]
-  uint32_t* ubits = hist + 2048;                                       // [words] union bitmap
-  uint32_t* hbits = ubits + words;                                     // [words] this head's bitmap
-  const int cap = amb_cap(Pmax);
-  int* amb_idx = reinterpret_cast<int*>(hbits + words);                // [cap]
-  size_t off = ((size_t)Pmax + 2048 + 2 * words + cap) * 4;
-  off = (off + 7) & ~size_t(7);
-  double* amb_s = reinterpret_cast<double*>(smem + off);               // [cap]
-  double* terms = amb_s + cap;                                         // [16 warps][128]
-  __shared__ uint32_t tmp[40];
-  __shared__ int s_namb, s_cin;
-  __shared__ float s_m;
+  const int gp = threadIdx.x / kGroupThreads;
+  const Group grp{1 + gp, kGroupThreads, (int)threadIdx.x % kGroupThreads};
+  uint32_t* ubits = reinterpret_cast<uint32_t*>(smem);                                  // [words]
+  uint32_t* gbase = ubits + words + gp * (Pmax + 2048 + words);
+  uint32_t* keys = gbase;                                                                // [Pmax]
+  uint32_t* hist = keys + Pmax;                                                          // [2048]
+  uint32_t* hbits = hist + 2048;                                                         // [words]
+  size_t toff = ((size_t)words + kSelGroups * ((size_t)Pmax + 2048 + words)) * 4;
+  toff = (toff + 7) & ~size_t(7);
+  double* terms = reinterpret_cast<double*>(smem + toff) + (threadIdx.x >> 5) * kHeadDim;  // [16 warps][128]
+  SelGroupSmem& gs = GS[gp];
 
   for (int i = threadIdx.x; i < words; i += blockDim.x) ubits[i] = 0;
   const int k = min(P, prm.budget_pages);
@@ -160,71 +180,71 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
     if (buf.head_page_bits) {
       for (int g = 0; g < G; ++g)
         for (int i = threadIdx.x; i < words; i += blockDim.x) {
-          int lo = i * 32;
-          uint32_t w = lo + 32 <= P ? 0xffffffffu : (lo >= P ? 0u : ((1u << (P - lo)) - 1u));
+          const int lo = i * 32;
+          const uint32_t w = lo + 32 <= P ? 0xffffffffu : (lo >= P ? 0u : ((1u << (P - lo)) - 1u));
           buf.head_page_bits[((size_t)unit * G + g) * words + i] = w;
         }
     }
   } else {
     const float amax = kv.kabsmax[unit];
-    for (int g = 0; g < G; ++g) {
-      const T* qh = q + ((size_t)unit * G + g) * kHeadDim;
-      const float* sc = buf.page_scores + ((size_t)unit * G + g) * Pmax;
-      // margin: ||q||_1 * max|k| * 300 u  (+ relative slack so fp64 divide ties are rescored)
-      float qa = 0.f;
-      if (threadIdx.x < 32)
-        for (int c = threadIdx.x; c < kHeadDim; c += 32) qa += fabsf(Elem<T>::to_f(qh[c]));
-      if (threadIdx.x < 32) {
+    const int wig = grp.warp(), lane = threadIdx.x & 31;
+    for (int g = gp; g < G; g += kSelGroups) {
+      const size_t qhi = (size_t)unit * G + g;
+      const T* qh = q + qhi * kHeadDim;
+      const float* sc = buf.page_scores + qhi * Pmax;
+      int* band_idx = buf.band_idx + qhi * Pmax;
+      double* band_s = buf.band_scores + qhi * Pmax;
+      // margin: ||q||_1 * max|k| * 300 u  (+ relative slack so fp64-divide ties are rescored)
+      if (wig == 0) {
+        float qa = 0.f;
+        for (int c = lane; c < kHeadDim; c += 32) qa += fabsf(Elem<T>::to_f(qh[c]));
         qa = warp_sum(qa);
-        if (threadIdx.x == 0) { s_m = qa * amax * (300.0f / 16777216.0f); s_namb = 0; s_cin = 0; }
+        if (lane == 0) { gs.margin = qa * amax * (300.0f / 16777216.0f); gs.namb = 0; gs.cin = 0; }
       }
-      for (int i = threadIdx.x; i < words; i += blockDim.x) hbits[i] = 0;
-      for (int i = threadIdx.x; i < P; i += blockDim.x) keys[i] = f2key(sc[i]);
-      __syncthreads();
-      const float t = key2f(block_kth_largest(keys, P, (uint32_t)k, hist, tmp));
-      const float m2 = 2.f * s_m + 1e-6f * fabsf(t) + 1e-30f;
+      for (int i = grp.tid; i < words; i += grp.nthreads) hbits[i] = 0;
+      for (int i = grp.tid; i < P; i += grp.nthreads) keys[i] = f2key(__ldcg(sc + i));
+      grp.sync();
+      const float t = key2f(group_kth_largest(grp, keys, P, (uint32_t)k, hist, gs.tmp, gs.res));
+      const float m2 = 2.f * gs.margin + 1e-6f * fabsf(t) + 1e-30f;
       const float hi_cut = t + m2, lo_cut = t - m2;
-      // classify
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+      for (int i = grp.tid; i < P; i += grp.nthreads) {
         const float s = key2f(keys[i]);
         if (s > hi_cut) {
           atomicOr(&hbits[i >> 5], 1u << (i & 31));
-          atomicAdd(&s_cin, 1);
+          atomicAdd(&gs.cin, 1);
         } else if (s >= lo_cut) {
-          int slot = atomicAdd(&s_namb, 1);
-          if (slot < cap) amb_idx[slot] = i;
-          else buf.counters[7] = 1;  // band overflow: flagged, checked by the host in debug runs
+          band_idx[atomicAdd(&gs.namb, 1)] = i;
         }
       }
-      __syncthreads();
-      const int namb = min(s_namb, cap);
-      const int need = k - s_cin;
-      // exact fp64 rescoring of the ambiguous band, one warp per page
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      for (int a = warp; a < namb; a += blockDim.x / 32) {
-        const int lp = amb_idx[a];
+      grp.sync();
+      const int namb = gs.namb;
+      const int need = k - gs.cin;
+      if (grp.tid == 0) atomicAdd(&buf.counters[1], (uint32_t)namb);  // diagnostic: rescored pages
+      // exact fp64 rescoring of the band, one warp per page
+      for (int a = wig; a < namb; a += grp.nwarps()) {
+        const int lp = band_idx[a];
         const T* lo = meta + ((size_t)pt[lp] * kv.num_kv_heads + h) * 2 * kHeadDim;
-        double s = exact_page_score<T>(qh, lo, lo + kHeadDim, terms + warp * kHeadDim);
-        if (lane == 0) amb_s[a] = s;
+        const double s = exact_page_score<T>(qh, lo, lo + kHeadDim, terms);
+        if (lane == 0) band_s[a] = s;
       }
-      __syncthreads();
+      grp.sync();
       // rank inside the band: (score desc, page asc); keep the best `need`
-      for (int a = threadIdx.x; a < namb; a += blockDim.x) {
-        const double sa = amb_s[a];
-        const int ia = amb_idx[a];
+      for (int a = grp.tid; a < namb; a += grp.nthreads) {
+        const double sa = band_s[a];
+        const int ia = band_idx[a];
         int rank = 0;
         for (int j = 0; j < namb; ++j) {
-          const double sj = amb_s[j];
-          rank += (sj > sa) || (sj == sa && amb_idx[j] < ia);
+          const double sj = band_s[j];
+          rank += (sj > sa) || (sj == sa && band_idx[j] < ia);
         }
         if (rank < need) atomicOr(&hbits[ia >> 5], 1u << (ia & 31));
       }
-      __syncthreads();
-      for (int i = threadIdx.x; i < words; i += blockDim.x) {
-        ubits[i] |= hbits[i];
-        if (buf.head_page_bits) buf.head_page_bits[((size_t)unit * G + g) * words + i] = hbits[i];
+      grp.sync();
+      for (int i = grp.tid; i < words; i += grp.nthreads) {
+        atomicOr(&ubits[i], hbits[i]);
+        if (buf.head_page_bits) buf.head_page_bits[qhi * words + i] = hbits[i];
       }
-      __syncthreads();
+      grp.sync();
     }
   }
   __syncthreads();
@@ -235,7 +255,7 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
     const int w = w0 + threadIdx.x;
     const uint32_t bits = w < words ? ubits[w] : 0u;
     uint32_t total;
-    const uint32_t incl = block_incl_scan(__popc(bits), tmp, total);
+    const uint32_t incl = block_incl_scan(__popc(bits), btmp, total);
     uint32_t pos = base + incl - __popc(bits);
     uint32_t x = bits;
     while (x) {
@@ -250,10 +270,9 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
 
 inline size_t select_smem_bytes(int Pmax) {
   const int words = (Pmax + 31) / 32;
-  const int cap = amb_cap(Pmax);
-  size_t bytes = ((size_t)Pmax + 2048 + 2 * words + cap) * 4;
+  size_t bytes = ((size_t)words + kSelGroups * ((size_t)Pmax + 2048 + words)) * 4;
   bytes = (bytes + 7) & ~size_t(7);
-  return bytes + (size_t)cap * 8 + (kSelThreads / 32) * kHeadDim * 8;
+  return bytes + (kSelThreads / 32) * kHeadDim * 8;
 }
 
 }  // namespace tw
@@ -288,7 +307,9 @@ extern "C" int tw_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
   if (!kv || !prm || !buf || kv->head_dim != kHeadDim || !buf->cand_pages || !buf->cand_count || !buf->counters)
     return TW_ERR_INVALID;
   if (prm->selector != TW_SELECT_FULL && prm->selector != TW_SELECT_QUEST) return TW_ERR_INVALID;
-  if (prm->selector == TW_SELECT_QUEST && (prm->budget_pages < 1 || !buf->page_scores || !q)) return TW_ERR_INVALID;
+  if (prm->selector == TW_SELECT_QUEST &&
+      (prm->budget_pages < 1 || !buf->page_scores || !buf->band_idx || !buf->band_scores || !q))
+    return TW_ERR_INVALID;
   return kv->dtype == TW_BF16 ? launch_select<__nv_bfloat16>(kv, q, prm, buf, stream)
                               : launch_select<float>(kv, q, prm, buf, stream);
 }

@@ -21,8 +21,27 @@
 // K3c: the group's final set is the union over its G heads (pipeline.py:347);
 // it is compacted in ascending token order and cut into attention work items.
 #include "block_scan.cuh"
+#ifdef TW_TOPP_TRACE
+#include <cstdio>
+#endif
 
 namespace tw {
+
+#ifdef TW_TOPP_TRACE
+__device__ unsigned long long g_trace[512 * 8];
+__device__ int g_trace_phase[512];
+#define TRACE(tag)                                                                                  \
+  do {                                                                                              \
+    if (threadIdx.x == 0 && blockIdx.x < 512) {                                                     \
+      unsigned long long now;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));                                      \
+      int ph = g_trace_phase[blockIdx.x]++;                                                         \
+      if (ph < 8) g_trace[blockIdx.x * 8 + ph] = now;                                               \
+    }                                                                                               \
+  } while (0)
+#else
+#define TRACE(tag) do {} while (0)
+#endif
 
 constexpr int kTopThreads = 512;
 constexpr int kBins = 4096;
@@ -34,6 +53,14 @@ __device__ __forceinline__ void atomic_add_u64_split(uint32_t* lo, uint32_t* hi,
   const uint32_t old = atomicAdd(lo, vlo);
   const uint32_t carry = (uint32_t)(old + vlo < old);
   if (vhi + carry) atomicAdd(hi, vhi + carry);
+}
+
+// Fixed-point softmax mass of logit z under max m: round(e * 2^sh) with
+// e = 2^((z - m) log2 e) on the SFU (rel. error ~1e-6 for z - m >= -40; the
+// scale is a power of two so the float->u64 conversion adds no error).
+__device__ __forceinline__ uint64_t mass_fx(float z, float m, float fscale) {
+  const float e = exp2f((z - m) * 1.4426950408889634f);
+  return __float2ull_rn(e * fscale);
 }
 
 __device__ __forceinline__ int dbin(float z, float m) {
@@ -127,207 +154,250 @@ __device__ __forceinline__ void find_crossing(TopSmem& S, double target, uint64_
   __syncthreads();
 }
 
-// One CTA per query head.
+// Vectorised walk over a head's logits: 4 x float4 in flight per thread.
+template <typename F>
+__device__ __forceinline__ void for_each_logit(const float* __restrict__ z, int npos, F&& f) {
+  const float4* z4 = reinterpret_cast<const float4*>(z);
+  const int n4 = npos >> 2;
+  for (int base = threadIdx.x; base < n4; base += blockDim.x * 4) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = base + u * blockDim.x;
+      v[u] = i < n4 ? __ldcg(z4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = base + u * blockDim.x;
+      if (i < n4) {
+        f(4 * i, v[u].x);
+        f(4 * i + 1, v[u].y);
+        f(4 * i + 2, v[u].z);
+        f(4 * i + 3, v[u].w);
+      }
+    }
+  }
+}
+
+// One CTA per query head; the last head of a unit to finish also forms the
+// group's final set (K3c) and reserves its attention work items.
 __global__ void __launch_bounds__(kTopThreads) topp_head_kernel(tw_paged_kv kv, tw_decode_params prm,
                                                                 tw_decode_buffers buf) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TopSmem& S = *reinterpret_cast<TopSmem*>(smem_raw);
+  __shared__ int s_last;
+  __shared__ uint32_t s_selc;
+  __shared__ unsigned long long s_selm;
   const int qh = blockIdx.x;
   const int G = kv.group_size;
   const int unit = qh / G;
   const int npos = buf.cand_count[unit] * kPage;
-  const float* z = buf.logits + (size_t)qh * kv.max_pages * kPage;
+  const size_t T = (size_t)kv.max_pages * kPage;
+  const float* z = buf.logits + (size_t)qh * T;
   const float M = key2f(buf.head_max[qh]);
   const double p_eff = fmin(prm.p, 1.0) - 1e-9;
   float* stats = buf.head_stats + (size_t)qh * 4;
-  if (p_eff <= 0.0 || npos == 0 || !(M > -INFINITY)) {
-    if (threadIdx.x == 0) {
-      buf.head_thr[qh] = 0xFFFFFFFFu;
-      stats[0] = 0.f; stats[1] = 0.f; stats[2] = 0.f; stats[3] = 0.f;
-    }
-    return;
-  }
-  // fixed-point scale: sums of up to npos terms stay below 2^63
-  const int lg = 32 - __clz(npos);
-  const double fscale = ldexp(1.0, 62 - lg);
-
-  for (int i = threadIdx.x; i < kBins; i += blockDim.x) { S.cnt[i] = 0; S.mlo[i] = 0; S.mhi[i] = 0; }
-  __syncthreads();
-  uint64_t zt = 0;
-  uint32_t nvalid = 0;
-  for (int i = threadIdx.x; i < npos; i += blockDim.x) {
-    const float zi = z[i];
-    if (zi == -INFINITY) continue;
-    ++nvalid;
-    const uint64_t mf = __double2ull_rn((double)exp_diff(zi, M) * fscale);
-    const int bb = dbin(zi, M);
-    atomicAdd(&S.cnt[bb], 1u);
-    if (mf) atomic_add_u64_split(&S.mlo[bb], &S.mhi[bb], mf);
-    zt += mf;
-  }
-  uint64_t Z;
-  block_incl_scan_u64(zt, S.scan_tmp, Z);  // total only
-  uint32_t b0;
-  block_incl_scan(nvalid, S.tmp32, b0);
-  const double target = p_eff * (double)Z;
-
-  // level 0: bins of (max - z), highest logit first (= ascending bin index)
-  find_crossing(S, target, 0, false);
-  int bin = S.bin;
-  uint64_t above_mass = S.above_mass;
-  uint32_t above_cnt = S.above_cnt;
-  uint32_t klo = 0, khi = 0xFFFFFFFFu;
-  if (bin < 0) {  // rounding: the whole set is needed
-    bin = kBins;  // sentinel: take everything
-  }
-  bool resolved = false;
-  uint32_t thr = 0;
-  if (bin == kBins) {
-    thr = 0;  // every valid token
-    resolved = true;
-  }
-  int members = bin < kBins ? (int)S.cnt[bin] : 0;
-  while (!resolved) {
+  uint32_t thr = 0xFFFFFFFFu;  // selects nothing
+  uint32_t b0 = 0;
+  uint64_t Z = 0;
+  float fscale = 1.f;
+  uint32_t sel_cnt = 0;        // |{z >= thr}|   (counted from the histograms, no extra pass)
+  uint64_t sel_mass = 0;       // its fixed-point mass
+  const bool empty = p_eff <= 0.0 || npos == 0 || !(M > -INFINITY);
+  TRACE("start");
+  if (!empty) {
+    // fixed-point scale: sums of up to npos terms stay below 2^63
+    const int lg = 32 - __clz(npos);
+    fscale = ldexpf(1.f, 62 - lg);
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) { S.cnt[i] = 0; S.mlo[i] = 0; S.mhi[i] = 0; }
     __syncthreads();
-    if (members <= kRankCap) {
-      // compact the members, then rank them exactly
-      if (threadIdx.x == 0) S.nmem = 0;
-      __syncthreads();
-      for (int i = threadIdx.x; i < npos; i += blockDim.x) {
-        const float zi = z[i];
-        if (zi == -INFINITY || dbin(zi, M) != bin) continue;
-        const uint32_t k = f2key(zi);
-        if (k < klo || k > khi) continue;
-        const int slot = atomicAdd(&S.nmem, 1);
-        if (slot < kRankCap) {
-          S.mkey[slot] = k;
-          S.mmass[slot] = __double2ull_rn((double)exp_diff(zi, M) * fscale);
-        }
-      }
-      __syncthreads();
-      const int nm = min(S.nmem, kRankCap);
-      if (threadIdx.x == 0) S.thr = 0;  // fallback: everything in range
-      __syncthreads();
-      for (int a = threadIdx.x; a < nm; a += blockDim.x) {
-        const uint32_t ka = S.mkey[a];
-        uint64_t above = 0, eq = 0;
-        for (int j = 0; j < nm; ++j) {
-          const uint32_t kj = S.mkey[j];
-          const uint64_t mj = S.mmass[j];
-          above += kj > ka ? mj : 0;
-          eq += kj == ka ? mj : 0;
-        }
-        if ((double)(above_mass + above) < target && target <= (double)(above_mass + above + eq))
-          S.thr = ka;  // every writer of this class writes the same key
-      }
-      __syncthreads();
-      thr = S.thr;
-      if (thr == 0) thr = klo;  // not reached (rounding): keep the whole range
+    uint64_t zt = 0;
+    uint32_t nvalid = 0;
+    for_each_logit(z, npos, [&](int, float zi) {
+      if (zi == -INFINITY) return;
+      ++nvalid;
+      const uint64_t mf = mass_fx(zi, M, fscale);
+      const int bb = dbin(zi, M);
+      atomicAdd(&S.cnt[bb], 1u);
+      if (mf) atomic_add_u64_split(&S.mlo[bb], &S.mhi[bb], mf);
+      zt += mf;
+    });
+    TRACE("pass1");
+    block_incl_scan_u64(zt, S.scan_tmp, Z);
+    block_incl_scan(nvalid, S.tmp32, b0);
+    const double target = p_eff * (double)Z;
+
+    // level 0: bins of (max - z), highest logit first (= ascending bin index)
+    find_crossing(S, target, 0, false);
+    TRACE("crossing");
+    int bin = S.bin;
+    uint64_t above_mass = S.above_mass;
+    uint32_t above_cnt = S.above_cnt;
+    uint32_t klo = 0, khi = 0xFFFFFFFFu;
+    bool resolved = false;
+    if (bin < 0) {  // rounding: the whole set is needed
+      thr = 0;
+      sel_cnt = b0;
+      sel_mass = Z;
       resolved = true;
-    } else {
-      // split the range by key: min/max key of the members, 4096 key bins
-      if (threadIdx.x == 0) { S.kmin = 0xFFFFFFFFu; S.kmax = 0; }
-      for (int i = threadIdx.x; i < kBins; i += blockDim.x) { S.cnt[i] = 0; S.mlo[i] = 0; S.mhi[i] = 0; }
+    }
+    int members = resolved ? 0 : (int)S.cnt[bin];
+    uint64_t range_mass = resolved ? 0 : (((uint64_t)S.mhi[bin] << 32) | S.mlo[bin]);
+    while (!resolved) {
       __syncthreads();
-      for (int i = threadIdx.x; i < npos; i += blockDim.x) {
-        const float zi = z[i];
-        if (zi == -INFINITY || dbin(zi, M) != bin) continue;
-        const uint32_t k = f2key(zi);
-        if (k < klo || k > khi) continue;
-        atomicMin(&S.kmin, k);
-        atomicMax(&S.kmax, k);
-      }
-      __syncthreads();
-      const uint32_t kmin = S.kmin, kmax = S.kmax;
-      if (kmin == kmax) {  // one tie class fills the bin: it is the threshold
-        thr = kmin;
+      if (members <= kRankCap) {
+        // compact the members, then rank them exactly
+        if (threadIdx.x == 0) { S.nmem = 0; s_selc = 0; s_selm = 0; }
+        __syncthreads();
+        for_each_logit(z, npos, [&](int, float zi) {
+          if (zi == -INFINITY || dbin(zi, M) != bin) return;
+          const uint32_t k = f2key(zi);
+          if (k < klo || k > khi) return;
+          const int slot = atomicAdd(&S.nmem, 1);
+          if (slot < kRankCap) {
+            S.mkey[slot] = k;
+            S.mmass[slot] = mass_fx(zi, M, fscale);
+          }
+        });
+        __syncthreads();
+        TRACE("members");
+        const int nm = min(S.nmem, kRankCap);
+        if (threadIdx.x == 0) S.thr = klo;  // fallback (rounding): keep the whole range
+        __syncthreads();
+        for (int a = threadIdx.x; a < nm; a += blockDim.x) {
+          const uint32_t ka = S.mkey[a];
+          uint64_t above = 0, eq = 0;
+          for (int j = 0; j < nm; ++j) {
+            const uint32_t kj = S.mkey[j];
+            const uint64_t mj = S.mmass[j];
+            above += kj > ka ? mj : 0;
+            eq += kj == ka ? mj : 0;
+          }
+          if ((double)(above_mass + above) < target && target <= (double)(above_mass + above + eq))
+            S.thr = ka;  // every writer of this class writes the same key
+        }
+        __syncthreads();
+        thr = S.thr;
+        for (int a = threadIdx.x; a < nm; a += blockDim.x)
+          if (S.mkey[a] >= thr) {
+            atomicAdd(&s_selc, 1u);
+            atomicAdd(&s_selm, (unsigned long long)S.mmass[a]);
+          }
+        __syncthreads();
+        TRACE("ranked");
+        sel_cnt = above_cnt + s_selc;
+        sel_mass = above_mass + s_selm;
         resolved = true;
-        break;
+      } else {
+        // split the range by key: min/max key of the members, 4096 key bins
+        if (threadIdx.x == 0) { S.kmin = 0xFFFFFFFFu; S.kmax = 0; }
+        for (int i = threadIdx.x; i < kBins; i += blockDim.x) { S.cnt[i] = 0; S.mlo[i] = 0; S.mhi[i] = 0; }
+        __syncthreads();
+        for_each_logit(z, npos, [&](int, float zi) {
+          if (zi == -INFINITY || dbin(zi, M) != bin) return;
+          const uint32_t k = f2key(zi);
+          if (k < klo || k > khi) return;
+          atomicMin(&S.kmin, k);
+          atomicMax(&S.kmax, k);
+        });
+        __syncthreads();
+        const uint32_t kmin = S.kmin, kmax = S.kmax;
+        if (kmin == kmax) {  // one tie class fills the range: it is the threshold
+          thr = kmin;
+          sel_cnt = above_cnt + members;
+          sel_mass = above_mass + range_mass;
+          break;
+        }
+        const int sh = max(0, (32 - __clz(kmax - kmin)) - 12);
+        for_each_logit(z, npos, [&](int, float zi) {
+          if (zi == -INFINITY || dbin(zi, M) != bin) return;
+          const uint32_t k = f2key(zi);
+          if (k < klo || k > khi) return;
+          const int sb = (int)((k - kmin) >> sh);
+          atomicAdd(&S.cnt[sb], 1u);
+          const uint64_t mf = mass_fx(zi, M, fscale);
+          if (mf) atomic_add_u64_split(&S.mlo[sb], &S.mhi[sb], mf);
+        });
+        __syncthreads();
+        find_crossing(S, target, above_mass, true);  // highest key first
+        if (S.bin < 0) {
+          thr = kmin;
+          sel_cnt = above_cnt + members;
+          sel_mass = above_mass + range_mass;
+          break;
+        }
+        const int sb = S.bin;
+        above_mass = S.above_mass;
+        above_cnt += S.above_cnt;
+        members = (int)S.cnt[sb];
+        range_mass = ((uint64_t)S.mhi[sb] << 32) | S.mlo[sb];
+        klo = kmin + ((uint32_t)sb << sh);
+        khi = min(kmax, klo + ((1u << sh) - 1u));
       }
-      const uint32_t span = kmax - kmin;
-      const int sh = max(0, (32 - __clz(span)) - 12);
-      for (int i = threadIdx.x; i < npos; i += blockDim.x) {
-        const float zi = z[i];
-        if (zi == -INFINITY || dbin(zi, M) != bin) continue;
-        const uint32_t k = f2key(zi);
-        if (k < klo || k > khi) continue;
-        const int sb = (int)((k - kmin) >> sh);
-        atomicAdd(&S.cnt[sb], 1u);
-        const uint64_t mf = __double2ull_rn((double)exp_diff(zi, M) * fscale);
-        if (mf) atomic_add_u64_split(&S.mlo[sb], &S.mhi[sb], mf);
+    }
+    __syncthreads();
+  }
+  TRACE("resolved");
+  // selection bitmap of the head's pruned set {z >= thr} (key compares only)
+  uint32_t* bits = buf.sel_bits + (size_t)qh * (T / 32);
+  {
+    const float4* z4 = reinterpret_cast<const float4*>(z);
+    const int n4 = npos >> 2;
+    const int lane = threadIdx.x & 31;
+    for (int i0 = 0; i0 < n4; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      uint32_t nib = 0;
+      if (i < n4) {
+        const float4 v = __ldcg(z4 + i);
+        nib = (v.x != -INFINITY && f2key(v.x) >= thr ? 1u : 0u) | (v.y != -INFINITY && f2key(v.y) >= thr ? 2u : 0u) |
+              (v.z != -INFINITY && f2key(v.z) >= thr ? 4u : 0u) | (v.w != -INFINITY && f2key(v.w) >= thr ? 8u : 0u);
       }
-      __syncthreads();
-      // highest key first
-      find_crossing(S, target, above_mass, true);
-      if (S.bin < 0) {  // rounding: keep the whole range
-        thr = kmin;
-        resolved = true;
-        break;
-      }
-      const int sb = S.bin;
-      above_cnt += S.above_cnt;
-      above_mass = S.above_mass;
-      members = (int)S.cnt[sb];
-      klo = kmin + ((uint32_t)sb << sh);
-      khi = (sh >= 32) ? kmax : min(kmax, klo + ((1u << sh) - 1u));
+      uint32_t w = nib << (4 * (lane & 7));
+      w |= __shfl_xor_sync(0xffffffffu, w, 1);
+      w |= __shfl_xor_sync(0xffffffffu, w, 2);
+      w |= __shfl_xor_sync(0xffffffffu, w, 4);
+      if ((lane & 7) == 0 && i < n4) bits[i >> 3] = w;
     }
   }
-  __syncthreads();
-  // statistics of the head's pruned set {z >= thr}
-  if (threadIdx.x == 0) { S.sel_cnt = 0; S.sel_mass = 0; }
-  __syncthreads();
-  uint32_t c = 0;
-  uint64_t ms = 0;
-  for (int i = threadIdx.x; i < npos; i += blockDim.x) {
-    const float zi = z[i];
-    if (zi == -INFINITY || f2key(zi) < thr) continue;
-    ++c;
-    ms += __double2ull_rn((double)exp_diff(zi, M) * fscale);
-  }
-  uint32_t ctot;
-  block_incl_scan(c, S.tmp32, ctot);
-  uint64_t mtot;
-  block_incl_scan_u64(ms, S.scan_tmp, mtot);
   if (threadIdx.x == 0) {
     buf.head_thr[qh] = thr;
-    stats[0] = (float)ctot;
-    stats[1] = (float)((double)mtot / (double)Z);
-    stats[2] = (float)((double)exp_diff(key2f(thr), M) * fscale / (double)Z);
+    stats[0] = (float)sel_cnt;
+    stats[1] = empty ? 0.f : (float)((double)sel_mass / (double)Z);
+    stats[2] = empty ? 0.f : (float)((double)mass_fx(key2f(thr), M, fscale) / (double)Z);
     stats[3] = (float)b0;
   }
-}
-
-// K3c: union of the G pruned sets, ascending token ids, attention work items.
-__global__ void __launch_bounds__(kTopThreads) group_union_kernel(tw_paged_kv kv, tw_decode_params prm,
-                                                                  tw_decode_buffers buf) {
-  __shared__ uint32_t tmp[40];
-  __shared__ uint32_t thr[8];
-  const int unit = blockIdx.x;
-  const int G = kv.group_size;
-  const int npos = buf.cand_count[unit] * kPage;
-  const size_t T = (size_t)kv.max_pages * kPage;
-  if (threadIdx.x < G) thr[threadIdx.x] = buf.head_thr[(size_t)unit * G + threadIdx.x];
+  TRACE("bitmap");
+  // ---- K3c: the last head of the unit forms the group set
+  __threadfence();
   __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(buf.unit_done + unit, 1) == G - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
   const int* cand = buf.cand_pages + (size_t)unit * kv.max_pages;
   int* out = buf.final_idx + (size_t)unit * T;
+  const int words = (npos + 31) >> 5;
+  const uint32_t* hb = buf.sel_bits + (size_t)unit * G * (T / 32);
   uint32_t base = 0;
-  for (int p0 = 0; p0 < npos; p0 += blockDim.x) {
-    const int pos = p0 + threadIdx.x;
-    uint32_t sel = 0;
-    if (pos < npos) {
-      for (int g = 0; g < G; ++g) {
-        const float zi = buf.logits[((size_t)unit * G + g) * T + pos];
-        if (zi != -INFINITY && f2key(zi) >= thr[g]) { sel = 1; break; }
-      }
-    }
+  for (int w0 = 0; w0 < words; w0 += blockDim.x) {
+    const int w = w0 + threadIdx.x;
+    uint32_t x = 0;
+    if (w < words)
+      for (int g = 0; g < G; ++g) x |= __ldcg(hb + (size_t)g * (T / 32) + w);
     uint32_t total;
-    const uint32_t incl = block_incl_scan(sel, tmp, total);
-    if (sel) out[base + incl - 1] = cand[pos >> 4] * kPage + (pos & 15);
+    const uint32_t incl = block_incl_scan(__popc(x), S.tmp32, total);
+    uint32_t pos = base + incl - __popc(x);
+    while (x) {
+      const int bit = __ffs(x) - 1;
+      x &= x - 1;
+      const int pp = w * 32 + bit;
+      out[pos++] = cand[pp >> 4] * kPage + (pp & 15);
+    }
     base += total;
   }
   if (threadIdx.x == 0) {
     buf.final_count[unit] = (int)base;
-    const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : 64;
+    const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : TW_DEFAULT_CHUNK;
     const int nitems = ((int)base + chunk - 1) / chunk;
     const int first = nitems ? (int)atomicAdd(&buf.counters[0], (uint32_t)nitems) : 0;
     buf.unit_items[2 * unit] = first;
@@ -410,6 +480,16 @@ __global__ void __launch_bounds__(256) topp_bisect_kernel(const double* __restri
 
 using namespace tw;
 
+#ifdef TW_TOPP_TRACE
+extern "C" int tw_debug_trace(unsigned long long* host_out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host_out, g_trace, sizeof(g_trace));
+  int zeros[512] = {0};
+  cudaMemcpyToSymbol(g_trace_phase, zeros, sizeof(zeros));
+  return 0;
+}
+#endif
+
 extern "C" int tw_topp(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,
                        cudaStream_t stream) {
   if (!kv || !prm || !buf || !buf->logits || !buf->head_thr || !buf->head_stats || !buf->final_idx ||
@@ -417,10 +497,11 @@ extern "C" int tw_topp(const tw_paged_kv* kv, const tw_decode_params* prm, const
     return TW_ERR_INVALID;
   if (!(prm->p >= 0.0 && prm->p <= 1.0)) return TW_ERR_INVALID;
   const int units = kv->num_seqs * kv->num_kv_heads;
+  if (!buf->sel_bits || !buf->unit_done) return TW_ERR_INVALID;
   const size_t smem = sizeof(TopSmem);
   cudaFuncSetAttribute(topp_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaMemsetAsync(buf->unit_done, 0, sizeof(int32_t) * units, stream);
   topp_head_kernel<<<units * kv->group_size, kTopThreads, smem, stream>>>(*kv, *prm, *buf);
-  group_union_kernel<<<units, kTopThreads, 0, stream>>>(*kv, *prm, *buf);
   return launch_status();
 }
 

@@ -157,7 +157,7 @@ class DecodeStats:
 class DecodeBuffers:
     """Caller-owned intermediate buffers of one decode step (tw_decode_buffers)."""
 
-    def __init__(self, cache: PagedKVCache, chunk_tokens: int = 64, head_page_bits: bool = False):
+    def __init__(self, cache: PagedKVCache, chunk_tokens: int = L.DEFAULT_CHUNK, head_page_bits: bool = False):
         dev = cache.device
         U = cache.num_seqs * cache.num_kv_heads
         Hq = U * cache.group_size
@@ -179,10 +179,14 @@ class DecodeBuffers:
         self.partials = torch.empty(self.max_items, G, L.HEAD_DIM + 2, dtype=torch.float32, device=dev)
         words = -(-cache.max_pages // 32)
         self.head_page_bits = torch.zeros(Hq, words, dtype=torch.int32, device=dev) if head_page_bits else None
+        self.sel_bits = torch.zeros(Hq, T // 32, dtype=torch.int32, device=dev)
+        self.unit_done = torch.zeros(U, dtype=torch.int32, device=dev)
+        self.band_idx = torch.empty(Hq, cache.max_pages, dtype=torch.int32, device=dev)
+        self.band_scores = torch.empty(Hq, cache.max_pages, dtype=torch.float64, device=dev)
         s = L.TwDecodeBuffers()
         for name in ("page_scores", "cand_pages", "cand_count", "logits", "head_max", "head_thr", "head_stats",
                      "final_idx", "final_count", "unit_items", "work_items", "counters", "partials",
-                     "head_page_bits"):
+                     "head_page_bits", "sel_bits", "unit_done", "band_idx", "band_scores"):
             setattr(s, name, L.ptr(getattr(self, name)))
         s.max_items = self.max_items
         self._struct = s
@@ -204,13 +208,15 @@ class TwilightDecoder:
     """
 
     def __init__(self, cache: PagedKVCache, selector: str = "quest", budget=None, p: float = 0.95,
-                 chunk_tokens: int = 64, head_page_bits: bool = False):
+                 chunk_tokens: int = L.DEFAULT_CHUNK, head_page_bits: bool = False,
+                 bufs: DecodeBuffers | None = None):
         if selector not in ("quest", "full"):
             raise ValueError(f"selector {selector!r} is not on the accelerated path (quest | full)")
         if not 0.0 <= p <= 1.0:
             raise ValueError(f"p={p} outside [0, 1]")
         self.cache = cache
-        self.bufs = DecodeBuffers(cache, chunk_tokens, head_page_bits)
+        # buffers may be shared by decoders of layers with the same geometry
+        self.bufs = bufs if bufs is not None else DecodeBuffers(cache, chunk_tokens, head_page_bits)
         self.params = L.TwDecodeParams()
         self.params.selector = L.TW_SELECT_QUEST if selector == "quest" else L.TW_SELECT_FULL
         self.params.p = float(p)

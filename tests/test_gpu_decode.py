@@ -236,3 +236,29 @@ def test_decode_step_fused_matches_staged():
     torch.cuda.synchronize()
     assert a.seq_lens.tolist() == [901, 641]
     assert torch.equal(out_a, out_c)
+
+
+@pytest.mark.parametrize("tau", [0.25, 2.0])
+def test_k2_filter_bounds_within_margin_at_32k(tau):
+    """The fp32 filter bounds sit within the error bound the select kernel
+    assumes, so only a thin band of pages is rescored in fp64."""
+    import ctypes
+    B, H, G, n = 1, 2, 4, 32768
+    cache, batch = _cache(B, H, G, n, torch.bfloat16, [n], seed=21, tau=tau, extra_pages=0)
+    dec = TwilightDecoder(cache, "quest", budget=8192, p=0.95)
+    q = batch.q.contiguous()
+    dec.select(q)
+    exact = torch.empty(B * H * G, cache.max_pages, dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().tw_quest_scores(ctypes.byref(cache.struct()), _lib.ptr(q), _lib.ptr(exact),
+                                          _lib.stream_handle()), "tw_quest_scores")
+    torch.cuda.synchronize()
+    approx = dec.bufs.page_scores.double() / np.sqrt(128)
+    for u in range(B * H):
+        amax = float(cache.kabsmax.view(-1)[u])
+        for g in range(G):
+            qh = q[0, u * G + g].float()
+            margin = float(qh.abs().sum()) * amax * 300 / 2**24 / np.sqrt(128)
+            err = (approx[u * G + g] - exact[u * G + g]).abs().max().item()
+            assert err <= margin, (err, margin)
+    rescored = int(dec.bufs.counters[1])
+    assert rescored < 0.02 * B * H * G * cache.max_pages, rescored

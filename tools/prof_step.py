@@ -1,0 +1,56 @@
+"""One C2-shaped layer (or --config) run stage by stage, for ncu captures.
+
+    ncu --set full -k regex:attn_kernel -c 2 -o gpurun_out/attn python tools/prof_step.py
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from bench import CONFIGS, TAUS  # noqa: E402
+from paper_2502_02770_b200.decode import PagedKVCache, TwilightDecoder, pages_for  # noqa: E402
+from paper_2502_02770_b200.workload import make_batch, tau_schedule  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C2")
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--dense", action="store_true")
+ap.add_argument("--batch", type=int, default=0)
+args = ap.parse_args()
+cfg = CONFIGS[args.config]
+B = args.batch or cfg["B"]
+H, G, n = cfg["H"], cfg["G"], cfg["n"]
+torch.cuda.set_device(0)
+cache = PagedKVCache(B, H, G, pages_for(n), dtype=torch.bfloat16)
+batch = make_batch(B, H, G, n, torch.bfloat16, tau=tau_schedule(H, TAUS), seed=1)
+cache.prefill(batch.K[:, :, : n - 1], batch.V[:, :, : n - 1])
+dec = TwilightDecoder(cache, cfg["selector"], budget=cfg["budget"], p=cfg["p"])
+q = batch.q.contiguous()
+pos = torch.full((B,), n - 1, dtype=torch.int32, device="cuda")
+out = torch.empty(B, H * G, 128, device="cuda")
+for _ in range(args.reps):
+    cache.append(batch.k_new, batch.v_new, pos)
+    dec.select(q)
+    dec.estimate(q)
+    dec.topp()
+    dec.attend(q, out)
+    if args.dense:
+        dec.dense(q, out)
+torch.cuda.synchronize()
+if os.environ.get("TW_LIB_PATH"):
+    import ctypes
+    import numpy as np
+    from paper_2502_02770_b200 import _lib
+    buf = (ctypes.c_ulonglong * (512 * 8))()
+    _lib.lib().tw_debug_trace(buf)
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(512, 8).astype(np.int64)
+    d = np.diff(a, axis=1)
+    print("phase durations us (mean over heads):", (d.mean(axis=0) / 1000).round(2).tolist())
+    print("phase durations us (max):", (d.max(axis=0) / 1000).round(2).tolist())
+    print("kernel span us:", (a[:, 6].max() - a[:, 0].min()) / 1000)
+st = dec.stats()
+print("cand tokens/unit", float(st.cand_pages.float().mean()) * 16, "final/unit", float(st.group_b1.float().mean()),
+      "rescored pages", int(dec.bufs.counters[1]))
