@@ -37,7 +37,7 @@ extern "C" {
 
 #define TW_PAGE_SIZE 16
 #define TW_QBLOCK_BYTES 1152
-#define TW_DEFAULT_CHUNK 256 /* tokens per sparse-attention work item */
+#define TW_DEFAULT_CHUNK 512 /* tokens per sparse-attention work item */
 
 /* Status codes; the shim maps them to the reference's exceptions
  * (attention.py:30-36, pruner.py:67-76, quantcache.py:246-267). */

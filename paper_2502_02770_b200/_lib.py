@@ -19,7 +19,7 @@ TW_OK, TW_ERR_INVALID, TW_ERR_INDEX, TW_ERR_DEGENERATE, TW_ERR_CUDA = range(5)
 TW_F32, TW_BF16 = 0, 1
 TW_SELECT_FULL, TW_SELECT_QUEST = 0, 1
 PAGE_SIZE = 16
-DEFAULT_CHUNK = 256
+DEFAULT_CHUNK = 512
 QBLOCK_BYTES = 1152
 HEAD_DIM = 128
 

@@ -65,13 +65,6 @@ __device__ __forceinline__ ItemDesc get_item(const tw_paged_kv& kv, const tw_dec
   return d;
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -374,13 +367,16 @@ __global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const
   }
 }
 
-// Merge the split-KV partials of every unit with more than one item:
-// one CTA per unit; weights exp(m_i - M) first, then coalesced weighted sums.
+// Merge the split-KV partials of every unit with more than one item: one CTA
+// per unit; item weights exp(m_i - M) first, then each warp sums a strided
+// subset of the items with float4 loads (all independent, so the loads of a
+// warp are in flight together) and the warps' sums are added in shared memory.
 template <int G, bool DENSE>
 __global__ void __launch_bounds__(256) merge_kernel(tw_paged_kv kv, tw_decode_buffers buf, float* __restrict__ out,
                                                     int chunk, int max_chunks) {
   __shared__ float w[2048];
   __shared__ float Lsum[8];
+  __shared__ __align__(16) float red[8][G * kHeadDim];
   const int unit = blockIdx.x;
   int first, n;
   if (DENSE) {
@@ -393,9 +389,10 @@ __global__ void __launch_bounds__(256) merge_kernel(tw_paged_kv kv, tw_decode_bu
   }
   if (n <= 1) return;
   const float* P = buf.partials;
+  constexpr int kStride = G * (kHeadDim + 2);
   for (int x = threadIdx.x; x < G * n; x += blockDim.x) {
     const int g = x / n, i = x % n;
-    w[x] = P[((size_t)(first + i) * G + g) * (kHeadDim + 2) + kHeadDim];
+    w[x] = P[(size_t)(first + i) * kStride + g * (kHeadDim + 2) + kHeadDim];
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -407,27 +404,40 @@ __global__ void __launch_bounds__(256) merge_kernel(tw_paged_kv kv, tw_decode_bu
     for (int i = lane; i < n; i += 32) {
       const float mi = w[g * n + i];
       const float e = mi == -INFINITY ? 0.f : __expf(mi - M);
-      L += e * P[((size_t)(first + i) * G + g) * (kHeadDim + 2) + kHeadDim + 1];
+      L += e * P[(size_t)(first + i) * kStride + g * (kHeadDim + 2) + kHeadDim + 1];
       w[g * n + i] = e;
     }
     L = warp_sum(L);
     if (lane == 0) Lsum[g] = L;
   }
   __syncthreads();
-  for (int x = threadIdx.x; x < G * kHeadDim; x += blockDim.x) {
-    const int g = x / kHeadDim, c = x % kHeadDim;
-    float O = 0.f;
-    int i = 0;
-    for (; i + 8 <= n; i += 8) {
-      float v[8];
+  // lane owns channels 4*lane..4*lane+3 of every head; warp sums items warp, warp+8, ...
+  float acc[G][4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = P[((size_t)(first + i + u) * G + g) * (kHeadDim + 2) + c];
+  for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
+  for (int i = warp; i < n; i += 8) {
+    const float* pi = P + (size_t)(first + i) * kStride;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) O = fmaf(w[g * n + i + u], v[u], O);
+    for (int g = 0; g < G; ++g) {
+      const float wi = w[g * n + i];
+      const float2 a = *reinterpret_cast<const float2*>(pi + g * (kHeadDim + 2) + 4 * lane);
+      const float2 b = *reinterpret_cast<const float2*>(pi + g * (kHeadDim + 2) + 4 * lane + 2);
+      acc[g][0] = fmaf(wi, a.x, acc[g][0]);
+      acc[g][1] = fmaf(wi, a.y, acc[g][1]);
+      acc[g][2] = fmaf(wi, b.x, acc[g][2]);
+      acc[g][3] = fmaf(wi, b.y, acc[g][3]);
     }
-    for (; i < n; ++i) O = fmaf(w[g * n + i], P[((size_t)(first + i) * G + g) * (kHeadDim + 2) + c], O);
-    const float L = Lsum[g];
-    out[((size_t)unit * G + g) * kHeadDim + c] = L > 0.f ? O / L : 0.f;
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+    *reinterpret_cast<float4*>(&red[warp][g * kHeadDim + 4 * lane]) = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
+  __syncthreads();
+  for (int x = threadIdx.x; x < G * kHeadDim; x += blockDim.x) {
+    float O = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) O += red[k][x];
+    const float L = Lsum[x / kHeadDim];
+    out[(size_t)unit * G * kHeadDim + x] = L > 0.f ? O / L : 0.f;
   }
 }
 

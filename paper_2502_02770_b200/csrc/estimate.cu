@@ -7,192 +7,199 @@
 //
 // Why tensor cores here: per 72-byte token the estimate needs G*d = 512 MACs
 // (G=4).  At B200's measured 35 T FFMA/s (tools/microbench.cu) CUDA cores
-// would take longer than streaming the codes at HBM speed, so the
-// code-times-query product runs on legacy mma.sync (bf16, m16n8k16): a page is
-// exactly one 16-row A tile, the G heads (times 1 or 3 bf16 terms of q) are the
-// N columns.  Codes 0..15 are exact in bf16, products are exact, accumulation
-// is fp32 -- the arithmetic matches an fp32 FFMA dot product.
+// would take longer than streaming the codes at HBM speed.  The code-times-
+// query product runs on legacy integer MMA (mma.sync m16n8k32 u8 x s8 -> s32,
+// 1.1 POPS measured): a page is one 16-row A tile; q is a 22-bit fixed-point
+// vector split into three signed 8-bit digits (one MMA column block per digit),
+// so every product and sum is exact integer arithmetic and the only rounding
+// is q -> fixed point (2^-22 of max|q|).  Nibbles become u8 A operands with
+// one AND (+ one shift) per 8 codes, 4x fewer instructions than a bf16 expand.
 //
-// Fragment trick (no shared memory, no ldmatrix): lane (t = lane%4, r = lane/4)
-// loads the 16 contiguous bytes [16t, 16t+16) of rows r and r+8 of the page --
-// one fully coalesced 512-B LDG.128 per 8 rows, straight from the reference
-// byte layout.  The K dimension of the MMA is permuted so that each 32-bit
-// word of nibbles expands to bf16x2 A registers with one LOP3 (+ shift) and a
-// bf16 subtract of the 0x4300 magic; q's B fragments use the same permutation.
+// Fragment trick (no ldmatrix): lane (t = lane%4, r = lane/4) reads the 16
+// contiguous bytes [16t, 16t+16) of rows r and r+8 of the page -- the
+// reference's own byte layout, staged through a per-warp cp.async ring.  The
+// MMA's K order is permuted so the low nibbles of a 32-bit word are one A
+// register and the high nibbles another; q's B fragments use the same order.
 #include "common.cuh"
 
 namespace tw {
 
-constexpr int kEstPagesPerCta = 32;  // 4 warps x 8 pages
+constexpr int kEstPagesPerCta = 32;  // candidate pages per work item (one per lane)
 constexpr int kEstWarps = 4;
 
-__device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
-// (n_a, n_b) nibble pair of `w` at bit offsets (sh, sh+16) -> exact bf16x2
-__device__ __forceinline__ uint32_t nib2bf16(uint32_t w, int sh) {
-  uint32_t x = ((w >> sh) & 0x000F000Fu) | 0x43004300u;  // bf16(128 + n)
-  __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&x);
-  const __nv_bfloat162 off = __floats2bfloat162_rn(128.f, 128.f);
-  v = __hsub2(v, off);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
-__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+__device__ __forceinline__ void mma_u8s8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// channel that k-slot `slot` (0..15) of k-step s maps to for lane group t
-__device__ __forceinline__ int kslot_channel(int t, int s, int slot) {
-  const int m = s >> 1, hf = s & 1;
-  const int j = slot & 7;            // 0,1 -> first pair; 8,9 handled by caller
-  const int base = 32 * t + 8 * m + 2 * hf;
-  return base + (slot >= 8 ? 1 : 0) + ((j & 1) ? 4 : 0);
-}
+constexpr int kDigits = 3;         // q as 3 signed base-256 digits of a 22-bit fixed-point value
+constexpr int kEstStages = 4;      // pages in flight per warp (cp.async ring)
 
-template <typename T, int G, int TERMS>
-__global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv, const T* __restrict__ q,
-                                                                  tw_decode_buffers buf) {
-  const int unit = blockIdx.y;
-  const int ncand = buf.cand_count[unit];
-  const int c0 = blockIdx.x * kEstPagesPerCta;
-  if (c0 >= ncand) return;
-  const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
-  const int n = kv.seq_lens[b];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int t = lane & 3, r = lane >> 2;
-  const int T_stride = kv.max_pages * kPage;
-
-  // ---- B fragments: q of head n = r (lanes with r >= G carry zeros), split into TERMS bf16 parts
-  uint32_t bf[TERMS][8][2];
-  {
-    const T* qh = q + ((size_t)unit * G + (r < G ? r : 0)) * kHeadDim;
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      float v[4];
-      const int slots[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int sl = slots[e] - 2 * t;  // 0,1,8,9
-        v[e] = r < G ? Elem<T>::to_f(qh[kslot_channel(t, s, sl)]) : 0.f;
-      }
-#pragma unroll
-      for (int j = 0; j < TERMS; ++j) {
-        float hi[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          hi[e] = __bfloat162float(__float2bfloat16_rn(v[e]));
-          if (j + 1 < TERMS) v[e] -= hi[e];  // exact residual
-        }
-        bf[j][s][0] = bf16x2_bits(hi[0], hi[1]);
-        bf[j][s][1] = bf16x2_bits(hi[2], hi[3]);
-      }
-    }
-  }
-  // sum_c q_c of the two heads whose accumulator columns this lane holds
-  float sq[2] = {0.f, 0.f};
+// q fixed point + digit B fragments for the lane's B column (head r), and for
+// the lane's two accumulator columns (heads 2t, 2t+1): sum(q) and 2^-S.
+template <typename T, int G>
+__device__ __forceinline__ void estimate_prologue(const T* __restrict__ q, int unit, uint32_t (&bd)[kDigits][4][2],
+                                                  float (&sq)[2], float (&inv_scale)[2]) {
+  const int lane = threadIdx.x & 31, t = lane & 3, r = lane >> 2;
+  float my_maxabs = 0.f;
+  sq[0] = sq[1] = 0.f;
+  inv_scale[0] = inv_scale[1] = 1.f;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    const T* qh = q + ((size_t)unit * G + g) * kHeadDim + 4 * lane;
-    float s = (Elem<T>::to_f(qh[0]) + Elem<T>::to_f(qh[1])) + (Elem<T>::to_f(qh[2]) + Elem<T>::to_f(qh[3]));
+    const T* qg = q + ((size_t)unit * G + g) * kHeadDim + 4 * lane;
+    const float v0 = Elem<T>::to_f(qg[0]), v1 = Elem<T>::to_f(qg[1]), v2 = Elem<T>::to_f(qg[2]),
+                v3 = Elem<T>::to_f(qg[3]);
+    float s = (v0 + v1) + (v2 + v3);
+    float m = fmaxf(fmaxf(fabsf(v0), fabsf(v1)), fmaxf(fabsf(v2), fabsf(v3)));
     s = warp_sum(s);
-    if (g == 2 * t) sq[0] = s;
-    if (g == 2 * t + 1) sq[1] = s;
+    m = warp_max(m);
+    const int S = m > 0.f ? 21 - ilogbf(m) : 0;
+    if (g == r) my_maxabs = (float)S;
+    if (g == 2 * t) { sq[0] = s; inv_scale[0] = ldexpf(1.f, -S); }
+    if (g == 2 * t + 1) { sq[1] = s; inv_scale[1] = ldexpf(1.f, -S); }
   }
-  const float inv_sqrt_d = 0.08838834764831845f;  // float32(1/sqrt(128)), as quantcache.py:258
-  float run_max[2] = {-INFINITY, -INFINITY};
+  const int S = (int)my_maxabs;
+  const T* qh = q + ((size_t)unit * G + (r < G ? r : 0)) * kHeadDim;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t dig[kDigits] = {0u, 0u, 0u};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        // k-slot 4t+i (+16 for half 1) <-> channel 32t + 8j + 2i (+1)
+        const int ch = 32 * t + 8 * j + 2 * i + half;
+        int x = r < G ? __float2int_rn(ldexpf(Elem<T>::to_f(qh[ch]), S)) : 0;
+#pragma unroll
+        for (int k = 0; k < kDigits; ++k) {
+          const int d = k + 1 < kDigits ? ((x + 128) & 255) - 128 : x;  // balanced digit, last takes the rest
+          x = (x - d) >> 8;
+          dig[k] |= ((uint32_t)d & 255u) << (8 * i);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kDigits; ++k) bd[k][j][half] = dig[k];
+    }
+  }
+}
 
-  const int* cand = buf.cand_pages + (size_t)unit * kv.max_pages;
-  const int* pt = kv.page_table + (size_t)b * kv.max_pages;
-  const int cend = min(c0 + kEstPagesPerCta, ncand);
-  // all pages of this warp (ci = c0 + warp + 4*i, i < 8) are loaded up front:
-  // 16 x 16 B of codes + 8 params per lane in flight before the first MMA
-  constexpr int kPPW = kEstPagesPerCta / kEstWarps;
-  int lp_all = 0;
-  {
-    const int ci = c0 + warp + kEstWarps * lane;
-    if (lane < kPPW && ci < cend) lp_all = cand[ci];
-  }
-  uint4 lo4[kPPW], hi4[kPPW];
-  float prmv[kPPW];
+// Persistent warp workers over (unit, 32-candidate-page) items, chunk-major;
+// each warp streams its pages' 1152-B INT4 blocks through a 4-deep cp.async ring.
+template <typename T, int G>
+__global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv, const T* __restrict__ q,
+                                                                  tw_decode_buffers buf, int max_chunks) {
+  __shared__ __align__(128) uint8_t ring[kEstWarps][kEstStages][kQBlockBytes];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = lane & 3, r = lane >> 2;
+  const int gw = blockIdx.x * kEstWarps + warp, nw = gridDim.x * kEstWarps;
+  const int units = kv.num_seqs * kv.num_kv_heads;
+  const int T_stride = kv.max_pages * kPage;
+  const float inv_sqrt_d = 0.08838834764831845f;  // float32(1/sqrt(128)), as quantcache.py:258
+  uint8_t (*R)[kQBlockBytes] = ring[warp];
+  uint32_t bd[kDigits][4][2];
+  float sq[2], isc[2];
+  int cur_unit = -1;
+  float run_max[2] = {-INFINITY, -INFINITY};
+  auto flush_max = [&](int u) {
 #pragma unroll
-  for (int i = 0; i < kPPW; ++i) {
-    const int ci = c0 + warp + kEstWarps * i;
-    const int lpi = __shfl_sync(0xffffffffu, lp_all, i);
-    if (ci < cend) {
-      const uint8_t* qb = kv.kq + ((size_t)pt[lpi] * kv.num_kv_heads + h) * kQBlockBytes;
-      lo4[i] = ld_stream(qb + r * 64 + t * 16);
-      hi4[i] = ld_stream(qb + (r + 8) * 64 + t * 16);
-      prmv[i] = __ldg(reinterpret_cast<const float*>(qb + kCodeBytes) + lane);
+    for (int e = 0; e < 2; ++e) {
+      float mx = run_max[e];
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      const int g = 2 * t + e;
+      if (r == 0 && g < G && mx > -INFINITY) atomicMax(buf.head_max + (size_t)u * G + g, f2key(mx));
+      run_max[e] = -INFINITY;
     }
-  }
-#pragma unroll
-  for (int i = 0; i < kPPW; ++i) {
-    const int ci = c0 + warp + kEstWarps * i;
-    if (ci >= cend) break;
-    const int lp = __shfl_sync(0xffffffffu, lp_all, i);
-    // ---- MMA over the 8 k-steps
-    float acc[TERMS][4];
-#pragma unroll
-    for (int j = 0; j < TERMS; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-    const uint32_t wl[4] = {lo4[i].x, lo4[i].y, lo4[i].z, lo4[i].w};
-    const uint32_t wh[4] = {hi4[i].x, hi4[i].y, hi4[i].z, hi4[i].w};
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int m = s >> 1, sh = (s & 1) ? 8 : 0;
-      uint32_t a[4];
-      a[0] = nib2bf16(wl[m], sh);
-      a[1] = nib2bf16(wh[m], sh);
-      a[2] = nib2bf16(wl[m], sh + 4);
-      a[3] = nib2bf16(wh[m], sh + 4);
-#pragma unroll
-      for (int j = 0; j < TERMS; ++j) mma_bf16(acc[j], a, bf[j][s][0], bf[j][s][1]);
+  };
+  for (int it = gw; it < units * max_chunks; it += nw) {
+    const int unit = it % units;  // chunk-major: non-empty items come first, spread over all warps
+    const int c0 = (it / units) * kEstPagesPerCta;
+    const int ncand = buf.cand_count[unit];
+    if (c0 >= ncand) continue;
+    const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
+    const int n = kv.seq_lens[b];
+    const int np = min(kEstPagesPerCta, ncand - c0);
+    // candidate page -> physical block, one page per lane
+    int lp_l = 0;
+    const uint8_t* src_l = kv.kq;
+    if (lane < np) {
+      lp_l = buf.cand_pages[(size_t)unit * kv.max_pages + c0 + lane];
+      src_l = kv.kq + ((size_t)kv.page_table[(size_t)b * kv.max_pages + lp_l] * kv.num_kv_heads + h) * kQBlockBytes;
     }
-    // ---- epilogue: rows r and r+8, heads 2t and 2t+1
-    const float pv = prmv[i];
-    const float sc_r = __shfl_sync(0xffffffffu, pv, r), sc_r8 = __shfl_sync(0xffffffffu, pv, r + 8);
-    const float z_r = __shfl_sync(0xffffffffu, pv, 16 + r), z_r8 = __shfl_sync(0xffffffffu, pv, 24 + r);
-    float d[4];
+    auto issue = [&](int i) {
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, (unsigned long long)src_l, i));
+      uint8_t* dst = R[i % kEstStages];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      float x = acc[0][e];
+      for (int c = lane; c < kQBlockBytes / 16; c += 32) cp_async16(dst + 16 * c, src + 16 * c);
+    };
 #pragma unroll
-      for (int j = 1; j < TERMS; ++j) x += acc[j][e];
-      d[e] = x;
+    for (int i = 0; i < kEstStages - 1; ++i) {
+      if (i < np) issue(i);
+      cp_commit();
     }
-    const int tok_r = lp * kPage + r;
-    const bool v_r = tok_r < n, v_r8 = tok_r + 8 < n;
-    if (2 * t < G) {
+    if (unit != cur_unit) {
+      if (cur_unit >= 0) flush_max(cur_unit);
+      estimate_prologue<T, G>(q, unit, bd, sq, isc);
+      cur_unit = unit;
+    }
+    for (int i = 0; i < np; ++i) {
+      if (i + kEstStages - 1 < np) issue(i + kEstStages - 1);
+      cp_commit();
+      cp_wait<kEstStages - 1>();
+      __syncwarp();
+      const uint8_t* pg = R[i % kEstStages];
+      const uint4 lo4 = *reinterpret_cast<const uint4*>(pg + r * 64 + t * 16);
+      const uint4 hi4 = *reinterpret_cast<const uint4*>(pg + (r + 8) * 64 + t * 16);
+      const float pv = reinterpret_cast<const float*>(pg + kCodeBytes)[lane];
+      __syncwarp();
+      const int lp = __shfl_sync(0xffffffffu, lp_l, i);
+      int acc[kDigits][4];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int g = 2 * t + e;
-        if (g < G) {
-          float l0 = v_r ? fmaf(sc_r, d[e], z_r * sq[e]) * inv_sqrt_d : -INFINITY;
-          float l1 = v_r8 ? fmaf(sc_r8, d[2 + e], z_r8 * sq[e]) * inv_sqrt_d : -INFINITY;
-          float* lg = buf.logits + ((size_t)unit * G + g) * T_stride + (size_t)ci * kPage;
-          lg[r] = l0;
-          lg[r + 8] = l1;
-          run_max[e] = fmaxf(run_max[e], fmaxf(l0, l1));
+      for (int k = 0; k < kDigits; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0;
+      const uint32_t wl[4] = {lo4.x, lo4.y, lo4.z, lo4.w};
+      const uint32_t wh[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t a[4];
+        a[0] = wl[j] & 0x0F0F0F0Fu;         // row r,   channels 32t+8j + {0,2,4,6}
+        a[1] = wh[j] & 0x0F0F0F0Fu;         // row r+8
+        a[2] = (wl[j] >> 4) & 0x0F0F0F0Fu;  // row r,   channels 32t+8j + {1,3,5,7}
+        a[3] = (wh[j] >> 4) & 0x0F0F0F0Fu;  // row r+8
+#pragma unroll
+        for (int k = 0; k < kDigits; ++k) mma_u8s8(acc[k], a, bd[k][j][0], bd[k][j][1]);
+      }
+      // ---- epilogue: rows r and r+8, heads 2t and 2t+1
+      const float sc_r = __shfl_sync(0xffffffffu, pv, r), sc_r8 = __shfl_sync(0xffffffffu, pv, r + 8);
+      const float z_r = __shfl_sync(0xffffffffu, pv, 16 + r), z_r8 = __shfl_sync(0xffffffffu, pv, 24 + r);
+      float d[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        d[e] = fmaf((float)acc[2][e], 65536.f, fmaf((float)acc[1][e], 256.f, (float)acc[0][e])) * isc[e & 1];
+      const int tok_r = lp * kPage + r;
+      const bool v_r = tok_r < n, v_r8 = tok_r + 8 < n;
+      const int ci = c0 + i;
+      if (2 * t < G) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int g = 2 * t + e;
+          if (g < G) {
+            const float l0 = v_r ? fmaf(sc_r, d[e], z_r * sq[e]) * inv_sqrt_d : -INFINITY;
+            const float l1 = v_r8 ? fmaf(sc_r8, d[2 + e], z_r8 * sq[e]) * inv_sqrt_d : -INFINITY;
+            float* lg = buf.logits + ((size_t)unit * G + g) * T_stride + (size_t)ci * kPage;
+            lg[r] = l0;
+            lg[r + 8] = l1;
+            run_max[e] = fmaxf(run_max[e], fmaxf(l0, l1));
+          }
         }
       }
     }
+    cp_wait<0>();
   }
-  // per-head max over this warp -> global (ordered-key atomicMax)
-#pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    float mx = run_max[e];
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-    const int g = 2 * t + e;
-    if (r == 0 && g < G && mx > -INFINITY) atomicMax(buf.head_max + (size_t)unit * G + g, f2key(mx));
-  }
+  if (cur_unit >= 0) flush_max(cur_unit);
 }
 
 // ---------------------------------------------------------------- per-token API
@@ -232,15 +239,26 @@ __global__ void estimate_tokens_kernel(tw_paged_kv kv, int seq, int kvh, const T
 
 using namespace tw;
 
-template <typename T, int TERMS>
+template <typename T, int G>
+static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, cudaStream_t stream) {
+  const int max_chunks = (kv->max_pages + kEstPagesPerCta - 1) / kEstPagesPerCta;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, estimate_kernel<T, G>, kEstWarps * 32, 0);
+  const int items = kv->num_seqs * kv->num_kv_heads * max_chunks;
+  int grid = sms * (per_sm < 1 ? 1 : per_sm);
+  if (grid * kEstWarps > items) grid = (items + kEstWarps - 1) / kEstWarps;
+  estimate_kernel<T, G><<<grid, kEstWarps * 32, 0, stream>>>(*kv, q, *buf, max_chunks);
+}
+
+template <typename T>
 static int launch_estimate(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, cudaStream_t stream) {
-  const int units = kv->num_seqs * kv->num_kv_heads;
-  dim3 grid((kv->max_pages + kEstPagesPerCta - 1) / kEstPagesPerCta, units), block(kEstWarps * 32);
   switch (kv->group_size) {
-    case 1: estimate_kernel<T, 1, TERMS><<<grid, block, 0, stream>>>(*kv, q, *buf); break;
-    case 2: estimate_kernel<T, 2, TERMS><<<grid, block, 0, stream>>>(*kv, q, *buf); break;
-    case 4: estimate_kernel<T, 4, TERMS><<<grid, block, 0, stream>>>(*kv, q, *buf); break;
-    case 8: estimate_kernel<T, 8, TERMS><<<grid, block, 0, stream>>>(*kv, q, *buf); break;
+    case 1: launch_estimate_g<T, 1>(kv, q, buf, stream); break;
+    case 2: launch_estimate_g<T, 2>(kv, q, buf, stream); break;
+    case 4: launch_estimate_g<T, 4>(kv, q, buf, stream); break;
+    case 8: launch_estimate_g<T, 8>(kv, q, buf, stream); break;
     default: return TW_ERR_INVALID;
   }
   return launch_status();
@@ -251,8 +269,8 @@ extern "C" int tw_estimate(const tw_paged_kv* kv, const void* q, const tw_decode
   (void)prm;
   if (!kv || !q || !buf || kv->head_dim != kHeadDim || !buf->logits || !buf->head_max) return TW_ERR_INVALID;
   cudaMemsetAsync(buf->head_max, 0, sizeof(uint32_t) * kv->num_seqs * kv->num_kv_heads * kv->group_size, stream);
-  if (kv->dtype == TW_BF16) return launch_estimate<__nv_bfloat16, 1>(kv, (const __nv_bfloat16*)q, buf, stream);
-  return launch_estimate<float, 3>(kv, (const float*)q, buf, stream);
+  if (kv->dtype == TW_BF16) return launch_estimate<__nv_bfloat16>(kv, (const __nv_bfloat16*)q, buf, stream);
+  return launch_estimate<float>(kv, (const float*)q, buf, stream);
 }
 
 extern "C" int tw_estimate_tokens(const tw_paged_kv* kv, int32_t seq, int32_t kv_head, const void* q,

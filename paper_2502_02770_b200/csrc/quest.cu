@@ -24,56 +24,206 @@ constexpr int kFilterPagesPerCta = 64;
 
 // ---------------------------------------------------------------- filter pass
 
-// grid (ceil(max_pages/64), B*H_kv); 8 warps; 16 lanes per page, 8 channels per lane.
+// Persistent warp workers over (unit, 64-page) items, chunk-major.  Each warp
+// streams its pages' metadata (lo|hi, 512 B in bf16) through a 4-stage
+// cp.async ring of 2-page stages; a half-warp scores one page (16 lanes x 8
+// channels) for all G heads and reduces with shuffles.
+constexpr int kQfWarps = 4;
+constexpr int kQfStages = 4;
+
 template <typename T, int G>
-__global__ void __launch_bounds__(256) quest_filter_kernel(tw_paged_kv kv, const T* __restrict__ q,
-                                                           float* __restrict__ scores) {
-  const int unit = blockIdx.y;
-  const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
-  const int npages = (kv.seq_lens[b] + kPage - 1) / kPage;
-  const int p0 = blockIdx.x * kFilterPagesPerCta;
-  if (p0 >= npages) return;
+__global__ void __launch_bounds__(kQfWarps * 32) quest_filter_kernel(tw_paged_kv kv, const T* __restrict__ q,
+                                                                     float* __restrict__ scores, int max_chunks) {
+  __shared__ __align__(128) T ring[kQfWarps][kQfStages][2][2 * kHeadDim];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane & 15, half = lane >> 4;
+  const int gw = blockIdx.x * kQfWarps + warp, nw = gridDim.x * kQfWarps;
+  const int units = kv.num_seqs * kv.num_kv_heads;
+  constexpr int kPageBytes = 2 * kHeadDim * sizeof(T);
+  constexpr int kChunks = kPageBytes / 16;  // 32 (bf16) or 64 (fp32) per page
+  T (*R)[2][2 * kHeadDim] = ring[warp];
   float qr[G][8];
+  int cur_unit = -1;
+  for (int it = gw; it < units * max_chunks; it += nw) {
+    const int unit = it % units;
+    const int p0 = (it / units) * kFilterPagesPerCta;
+    const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
+    const int npages = (kv.seq_lens[b] + kPage - 1) / kPage;
+    if (p0 >= npages) continue;
+    const int np = min(kFilterPagesPerCta, npages - p0);
+    const int* pt = kv.page_table + (size_t)b * kv.max_pages;
+    // physical metadata blocks of pages p0 + lane and p0 + 32 + lane
+    const T* src0 = reinterpret_cast<const T*>(kv.kmeta);
+    const T* src1 = src0;
+    if (lane < np) src0 += ((size_t)pt[p0 + lane] * kv.num_kv_heads + h) * 2 * kHeadDim;
+    if (lane + 32 < np) src1 += ((size_t)pt[p0 + 32 + lane] * kv.num_kv_heads + h) * 2 * kHeadDim;
+    const int nst = (np + 1) / 2;
+    auto issue = [&](int s) {
 #pragma unroll
-  for (int g = 0; g < G; ++g) load8(q + ((size_t)unit * G + g) * kHeadDim + 8 * sub, qr[g]);
-  const int pend = min(p0 + kFilterPagesPerCta, npages);
-  const int* pt = kv.page_table + (size_t)b * kv.max_pages;
-  // 4 pages per half-warp, all loads issued before any math
-  constexpr int kU = kFilterPagesPerCta / 16;
-  float l8[kU][8], h8[kU][8];
+      for (int j = 0; j < 2; ++j) {
+        const int pg = 2 * s + j;
+        if (pg < np) {
+          const T* src = reinterpret_cast<const T*>(
+              __shfl_sync(0xffffffffu, (unsigned long long)(pg < 32 ? src0 : src1), pg & 31));
+          char* dst = reinterpret_cast<char*>(&R[s % kQfStages][j][0]);
 #pragma unroll
-  for (int u = 0; u < kU; ++u) {
-    const int lp = p0 + warp * 2 + half + 16 * u;
-    if (lp < pend) {
-      const int phys = pt[lp];
-      const T* lo = reinterpret_cast<const T*>(kv.kmeta) + ((size_t)phys * kv.num_kv_heads + h) * 2 * kHeadDim + 8 * sub;
-      load8(lo, l8[u]);
-      load8(lo + kHeadDim, h8[u]);
+          for (int c = lane; c < kChunks; c += 32)
+            cp_async16(dst + 16 * c, reinterpret_cast<const char*>(src) + 16 * c);
+        }
+      }
+    };
+#pragma unroll
+    for (int s = 0; s < kQfStages - 1; ++s) {
+      if (s < nst) issue(s);
+      cp_commit();
     }
+    if (unit != cur_unit) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) load8(q + ((size_t)unit * G + g) * kHeadDim + 8 * sub, qr[g]);
+      cur_unit = unit;
+    }
+    for (int s = 0; s < nst; ++s) {
+      if (s + kQfStages - 1 < nst) issue(s + kQfStages - 1);
+      cp_commit();
+      cp_wait<kQfStages - 1>();
+      __syncwarp();
+      const int pg = 2 * s + half;
+      float l8[8], h8[8];
+      load8(&R[s % kQfStages][half][8 * sub], l8);
+      load8(&R[s % kQfStages][half][kHeadDim + 8 * sub], h8);
+      __syncwarp();
+      float acc[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float a = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a = fmaf(qr[g][i], qr[g][i] >= 0.f ? h8[i] : l8[i], a);
+        acc[g] = a;
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
+      if (sub < G && pg < np) {
+        float v = acc[0];
+#pragma unroll
+        for (int g = 1; g < G; ++g) if (sub == g) v = acc[g];
+        scores[((size_t)unit * G + sub) * kv.max_pages + p0 + pg] = v;
+      }
+    }
+    cp_wait<0>();
   }
+}
+
+// bf16 metadata: the bound is linear in the metadata row (lo | hi):
+//   score = qneg . lo + qpos . hi,  qpos = max(q, 0), qneg = min(q, 0),
+// i.e. a [pages x 256] x [256 x heads] product -> legacy mma.sync m16n8k16
+// (bf16 products exact, fp32 accumulation, covered by the select margin).
+// Per warp: 16-page tiles (16 x 512 B, XOR-swizzled rows) through a 3-stage
+// cp.async ring; one ldmatrix.x4 + one MMA per page-tile k-step.
+constexpr int kQmStages = 3;
+
+__device__ __forceinline__ void ldsm_x4_q(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void mma_bf16_q(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int G>
+__global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_paged_kv kv,
+                                                                         const __nv_bfloat16* __restrict__ q,
+                                                                         float* __restrict__ scores, int max_chunks) {
+  extern __shared__ __align__(128) uint8_t qm_ring[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = lane & 3, r = lane >> 2, q8 = lane >> 3, rr = lane & 7;
+  const int gw = blockIdx.x * kQfWarps + warp, nw = gridDim.x * kQfWarps;
+  const int units = kv.num_seqs * kv.num_kv_heads;
+  uint8_t (*R)[16 * 512] = reinterpret_cast<uint8_t (*)[16 * 512]>(qm_ring + (size_t)warp * kQmStages * 16 * 512);
+  uint32_t qb[16][2];  // B fragments of [qneg ; qpos] for head column r
+  int cur_unit = -1;
+  for (int it = gw; it < units * max_chunks; it += nw) {
+    const int unit = it % units;
+    const int p0 = (it / units) * kFilterPagesPerCta;
+    const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
+    const int npages = (kv.seq_lens[b] + kPage - 1) / kPage;
+    if (p0 >= npages) continue;
+    const int np = min(kFilterPagesPerCta, npages - p0);
+    const int* pt = kv.page_table + (size_t)b * kv.max_pages;
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(kv.kmeta);
+    const uint8_t* src0 = base;
+    const uint8_t* src1 = base;
+    if (lane < np) src0 += ((size_t)pt[p0 + lane] * kv.num_kv_heads + h) * 512;
+    if (lane + 32 < np) src1 += ((size_t)pt[p0 + 32 + lane] * kv.num_kv_heads + h) * 512;
+    const int ntile = (np + 15) / 16;
+    auto issue = [&](int s) {
+      uint8_t* dst = R[s % kQmStages];
+#pragma unroll 4
+      for (int i = 0; i < 16; ++i) {
+        const int pg = 16 * s + i;
+        if (pg < np) {
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(
+              __shfl_sync(0xffffffffu, (unsigned long long)(pg < 32 ? src0 : src1), pg & 31));
+          // 32 chunks of 16 B per row; chunk c stored at c ^ (i & 7)
+          cp_async16(dst + i * 512 + ((lane ^ (i & 7)) << 4), src + 16 * lane);
+        }
+      }
+    };
 #pragma unroll
-  for (int u = 0; u < kU; ++u) {
-    const int lp = p0 + warp * 2 + half + 16 * u;
-    float acc[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float a = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a = fmaf(qr[g][i], qr[g][i] >= 0.f ? h8[u][i] : l8[u][i], a);
-      acc[g] = a;
+    for (int s = 0; s < kQmStages - 1; ++s) {
+      if (s < ntile) issue(s);
+      cp_commit();
     }
+    if (unit != cur_unit) {
+      const __nv_bfloat16* qh = q + ((size_t)unit * G + (r < G ? r : 0)) * kHeadDim;
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1)
+      for (int kk = 0; kk < 16; ++kk) {
+        // k = 16kk + {2t, 2t+1 | 2t+8, 2t+9}; k < 128 -> qneg[k], else qpos[k - 128]
 #pragma unroll
-      for (int g = 0; g < G; ++g) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
-    if (sub < G && lp < pend) {
-      float v = acc[0];
-#pragma unroll
-      for (int g = 1; g < G; ++g) if (sub == g) v = acc[g];
-      scores[((size_t)unit * G + sub) * kv.max_pages + lp] = v;
+        for (int hb = 0; hb < 2; ++hb) {
+          const int k0 = 16 * kk + 2 * t + 8 * hb;
+          const int c = k0 & 127;
+          float a = r < G ? __bfloat162float(qh[c]) : 0.f;
+          float bq = r < G ? __bfloat162float(qh[c + 1]) : 0.f;
+          if (kk < 8) { a = fminf(a, 0.f); bq = fminf(bq, 0.f); }
+          else { a = fmaxf(a, 0.f); bq = fmaxf(bq, 0.f); }
+          __nv_bfloat162 v = __floats2bfloat162_rn(a, bq);
+          qb[kk][hb] = *reinterpret_cast<uint32_t*>(&v);
+        }
+      }
+      cur_unit = unit;
     }
+    for (int s = 0; s < ntile; ++s) {
+      if (s + kQmStages - 1 < ntile) issue(s + kQmStages - 1);
+      cp_commit();
+      cp_wait<kQmStages - 1>();
+      __syncwarp();
+      const uint8_t* tile = R[s % kQmStages];
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const int row = (q8 & 1) * 8 + rr;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        uint32_t a[4];
+        const int chunk = 2 * kk + (q8 >> 1);
+        ldsm_x4_q(a, tile + row * 512 + ((chunk ^ (row & 7)) << 4));
+        mma_bf16_q(acc, a, qb[kk][0], qb[kk][1]);
+      }
+      __syncwarp();
+      // rows r, r+8 (pages), cols 2t, 2t+1 (heads)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int pg = 16 * s + r + (e >= 2 ? 8 : 0);
+        const int g = 2 * t + (e & 1);
+        if (g < G && pg < np) scores[((size_t)unit * G + g) * kv.max_pages + p0 + pg] = acc[e];
+      }
+    }
+    cp_wait<0>();
   }
 }
 
@@ -285,14 +435,44 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
   const int units = kv->num_seqs * kv->num_kv_heads;
   cudaMemsetAsync(buf->counters, 0, 8 * sizeof(uint32_t), stream);
   if (prm->selector == TW_SELECT_QUEST) {
-    dim3 grid((kv->max_pages + kFilterPagesPerCta - 1) / kFilterPagesPerCta, units);
+    const int max_chunks = (kv->max_pages + kFilterPagesPerCta - 1) / kFilterPagesPerCta;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int items = units * max_chunks;
     const T* qq = (const T*)q;
-    switch (kv->group_size) {
-      case 1: quest_filter_kernel<T, 1><<<grid, 256, 0, stream>>>(*kv, qq, buf->page_scores); break;
-      case 2: quest_filter_kernel<T, 2><<<grid, 256, 0, stream>>>(*kv, qq, buf->page_scores); break;
-      case 4: quest_filter_kernel<T, 4><<<grid, 256, 0, stream>>>(*kv, qq, buf->page_scores); break;
-      case 8: quest_filter_kernel<T, 8><<<grid, 256, 0, stream>>>(*kv, qq, buf->page_scores); break;
-      default: return TW_ERR_INVALID;
+    auto go = [&](auto kern) {
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQfWarps * 32, 0);
+      int grid = sms * (per_sm < 1 ? 1 : per_sm);
+      if (grid * kQfWarps > items) grid = (items + kQfWarps - 1) / kQfWarps;
+      kern<<<grid, kQfWarps * 32, 0, stream>>>(*kv, qq, buf->page_scores, max_chunks);
+    };
+    if constexpr (sizeof(T) == 2) {
+      auto gom = [&](auto kern) {
+        const int smem = kQfWarps * kQmStages * 16 * 512;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQfWarps * 32, smem);
+        int grid = sms * (per_sm < 1 ? 1 : per_sm);
+        if (grid * kQfWarps > items) grid = (items + kQfWarps - 1) / kQfWarps;
+        kern<<<grid, kQfWarps * 32, smem, stream>>>(*kv, (const __nv_bfloat16*)q, buf->page_scores, max_chunks);
+      };
+      switch (kv->group_size) {
+        case 1: gom(quest_filter_mma_kernel<1>); break;
+        case 2: gom(quest_filter_mma_kernel<2>); break;
+        case 4: gom(quest_filter_mma_kernel<4>); break;
+        case 8: gom(quest_filter_mma_kernel<8>); break;
+        default: return TW_ERR_INVALID;
+      }
+    } else {
+      switch (kv->group_size) {
+        case 1: go(quest_filter_kernel<T, 1>); break;
+        case 2: go(quest_filter_kernel<T, 2>); break;
+        case 4: go(quest_filter_kernel<T, 4>); break;
+        case 8: go(quest_filter_kernel<T, 8>); break;
+        default: return TW_ERR_INVALID;
+      }
     }
   }
   const size_t smem = select_smem_bytes(kv->max_pages);

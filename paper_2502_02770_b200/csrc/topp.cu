@@ -7,7 +7,7 @@
 // p_eff = min(p, sum w) - 1e-9 (break rules :99-104).  We compute that set
 // directly instead of bisecting (~50 passes): a mass-weighted radix select.
 //
-//   pass 1   e_i = exp(z_i - max) (fp32-accurate, exp_diff), quantised to
+//   pass 1   e_i = exp(z_i - max) (SFU exp2, ~1e-6 relative), quantised to
 //            u64 fixed point (exact, order-independent sums => deterministic);
 //            histogram of (count, mass) over 4096 bins of (max - z) ; the
 //            crossing bin is the first (highest-z) bin where the running mass

@@ -88,6 +88,26 @@ __global__ void hmma_k(float* out, const uint32_t* in) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void imma_k(int* out, const uint32_t* in) {
+  uint32_t a0 = in[threadIdx.x], a1 = in[threadIdx.x + 1], a2 = in[threadIdx.x + 2], a3 = in[threadIdx.x + 3];
+  uint32_t b0 = in[threadIdx.x + 4], b1 = in[threadIdx.x + 5];
+  int c[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) for (int t = 0; t < 4; ++t) c[j][t] = 0;
+#pragma unroll 4
+  for (int i = 0; i < ITERS / 8; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                   : "+r"(c[j][0]), "+r"(c[j][1]), "+r"(c[j][2]), "+r"(c[j][3])
+                   : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  }
+  int s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += c[j][0] + c[j][1] + c[j][2] + c[j][3];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __device__ __forceinline__ int4 ld_nc(const int4* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
@@ -153,7 +173,10 @@ int main() {
   printf(", \"dfma_tflops\": %.2f", 2.0 * blocks * threads * (ITERS / 4) * 8 / (t * 1e-3) / 1e12);
   t = timeit([&] { hmma_k<<<blocks, threads>>>(fo, ui); });
   printf(", \"hmma_bf16_tflops\": %.1f", 2.0 * 16 * 8 * 16 * (blocks * threads / 32) * (ITERS / 8) * 8 / (t * 1e-3) / 1e12);
+  t = timeit([&] { imma_k<<<blocks, threads>>>((int*)fo, ui); });
+  printf(", \"imma_u8s8_tops\": %.1f", 2.0 * 16 * 8 * 32 * (blocks * threads / 32) * (ITERS / 8) * 8 / (t * 1e-3) / 1e12);
   CK(cudaGetLastError());
+  fflush(stdout);
 
   size_t bytes = (size_t)4 << 30;
   int4* buf; CK(cudaMalloc(&buf, bytes)); CK(cudaMemset(buf, 1, bytes));
@@ -166,7 +189,7 @@ int main() {
     }
   }
   // per-SM bandwidth: one CTA on a few SMs only, each streaming its own 64 MB slice
-  for (int ncta : {1, 16, 64, 128}) {
+  for (int ncta : {1, 16, 32, 64}) {
     size_t sl = (size_t)ncta * (64 << 20) / 16;
     t = timeit([&] { stream_k<<<ncta, 1024>>>(buf, sl, io); });
     printf(", \"per_cta_gbs_n%d\": %.1f", ncta, sl * 16.0 / (t * 1e-3) / 1e9 / ncta);
