@@ -208,7 +208,7 @@ def run_ours(args, cfg):
     q, k_new, v_new = step_in.q.contiguous(), step_in.k_new.contiguous(), step_in.v_new.contiguous()
     positions = torch.full((B,), n - 1, dtype=torch.int32, device=dev)
     out = torch.empty(B, H_local * G, 128, dtype=torch.float32, device=dev)
-    gathered = torch.empty(world, B, H_local * G, 128, dtype=torch.float32, device=dev) if (
+    gathered = torch.empty(world * B, H_local * G, 128, dtype=torch.float32, device=dev) if (
         cfg["shard"] == "head" and world > 1) else None
 
     def step_once(i, which=None):

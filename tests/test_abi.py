@@ -1,0 +1,91 @@
+"""The C ABI (include/twilight.h) and its ctypes binding, checked on CPU:
+the library loads without a GPU, exports every declared symbol, and the
+ctypes structures have the C layout (compiled with gcc against the header)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2502_02770_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "twilight.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t)\s+(tw_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.lib()
+    decl = declared_symbols()
+    assert decl, "no declarations parsed"
+    assert sorted(_lib.EXPORTS) == decl
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert lib.tw_version() == 100
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for name in decl:
+        assert re.search(rf"\bT {name}\b", out), f"{name} not exported"
+
+
+def test_struct_layouts_match_header(tmp_path):
+    src = tmp_path / "sz.c"
+    src.write_text(
+        '#include "twilight.h"\n#include <stdio.h>\n#include <stddef.h>\n'
+        "int main(){printf(\"%zu %zu %zu %zu %zu %zu\\n\", sizeof(tw_paged_kv), sizeof(tw_decode_params),"
+        " sizeof(tw_decode_buffers), offsetof(tw_decode_params, p), offsetof(tw_decode_buffers, max_items),"
+        " offsetof(tw_paged_kv, seq_lens));return 0;}\n")
+    exe = tmp_path / "sz"
+    cuda_inc = "/usr/local/cuda/include"
+    r = subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-I", cuda_inc, str(src), "-o", str(exe)],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        pytest.skip(f"gcc/cuda headers unavailable: {r.stderr[:200]}")
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    want = [ctypes.sizeof(_lib.TwPagedKV), ctypes.sizeof(_lib.TwDecodeParams), ctypes.sizeof(_lib.TwDecodeBuffers),
+            _lib.TwDecodeParams.p.offset, _lib.TwDecodeBuffers.max_items.offset, _lib.TwPagedKV.seq_lens.offset]
+    assert got == want
+
+
+def test_invalid_arguments_are_rejected_without_a_gpu():
+    lib = _lib.lib()
+    # null geometry / bad sizes return TW_ERR_INVALID before touching the device
+    assert lib.tw_quant_append(None, None, None, None, None) == _lib.TW_ERR_INVALID
+    assert lib.tw_quant_rows(None, 0, 128, _lib.TW_BF16, 4, None, None, None, None) == _lib.TW_ERR_INVALID
+    assert lib.tw_quant_rows(None, 4, 128, _lib.TW_BF16, 3, None, None, None, None) == _lib.TW_ERR_INVALID
+    assert lib.tw_topp_bisect(None, 1, 4, 0.5, 1e-15, 64, None, None, None, None) == _lib.TW_ERR_INVALID
+    kv = _lib.TwPagedKV()
+    kv.num_seqs, kv.num_kv_heads, kv.group_size, kv.head_dim, kv.max_pages = 1, 1, 3, 128, 4
+    prm = _lib.TwDecodeParams()
+    buf = _lib.TwDecodeBuffers()
+    assert lib.tw_topp(ctypes.byref(kv), ctypes.byref(prm), ctypes.byref(buf), None) == _lib.TW_ERR_INVALID
+    assert lib.tw_max_work_items(ctypes.byref(kv), 512) == 1
+
+
+def test_status_codes_map_to_reference_exceptions():
+    _lib.check(_lib.TW_OK, "x")
+    with pytest.raises(ValueError):
+        _lib.check(_lib.TW_ERR_INVALID, "x")
+    with pytest.raises(IndexError):
+        _lib.check(_lib.TW_ERR_INDEX, "x")
+    with pytest.raises(_lib.DegenerateSelectionError):
+        _lib.check(_lib.TW_ERR_DEGENERATE, "x")
+    assert issubclass(_lib.DegenerateSelectionError, ValueError)
+    with pytest.raises(RuntimeError):
+        _lib.check(_lib.TW_ERR_CUDA, "x")
+
+
+def test_ops_refuse_cpu_tensors():
+    import torch
+
+    from paper_2502_02770_b200 import attention_weights, binary_search_top_p, BinarySearchConfig
+
+    with pytest.raises(ValueError):
+        attention_weights(torch.ones(128), torch.ones(4, 128))
+    with pytest.raises(ValueError):
+        binary_search_top_p(torch.full((4,), 0.25, dtype=torch.float64), BinarySearchConfig(p=0.5))
