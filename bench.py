@@ -456,6 +456,11 @@ _POOL_STATE = {}
 def _pool_init(cfg, n, seed):
     import numpy as np
     os.environ["OMP_NUM_THREADS"] = "1"
+    try:  # one BLAS thread per worker process (BLAS was initialised in the parent)
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
     from oracle import twilight_oracle as orc
     K, V, Q = _unit_arrays(cfg, n, seed % len(TAUS), seed)
     _POOL_STATE["unit"] = (K, V, Q, orc.prepare_unit(K))
