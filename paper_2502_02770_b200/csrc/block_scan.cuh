@@ -145,4 +145,86 @@ __device__ __forceinline__ uint32_t group_kth_largest(const Group& g, const uint
   return prefix;
 }
 
+// Same result as group_kth_largest, by a bitwise search over the informative
+// bits: for each bit, one counting pass over the keys (shared memory) and one
+// group reduction.  Cheaper than histogram passes when keys cluster.
+// `tmp` needs nwarps words.
+__device__ __forceinline__ uint32_t group_kth_largest_bs(const Group& g, const uint32_t* keys, int n, uint32_t k,
+                                                         uint32_t* tmp) {
+  uint32_t mn = 0xFFFFFFFFu, mx = 0;
+  for (int i = g.tid; i < n; i += g.nthreads) {
+    mn = min(mn, keys[i]);
+    mx = max(mx, keys[i]);
+  }
+  group_minmax_u32(g, mn, mx, tmp);
+  if (mn == mx) return mn;
+  const int hi = 31 - __clz(mn ^ mx);
+  uint32_t res = hi == 31 ? 0u : (mn & ~((2u << hi) - 1u));
+  for (int bit = hi; bit >= 0; --bit) {
+    const uint32_t cand = res | (1u << bit);
+    uint32_t c = 0;
+#pragma unroll 8
+    for (int i = g.tid; i < n; i += g.nthreads) c += keys[i] >= cand ? 1u : 0u;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((g.tid & 31) == 0) tmp[g.warp()] = c;
+    g.sync();
+    uint32_t tot = 0;
+    for (int w = 0; w < g.nwarps(); ++w) tot += tmp[w];
+    g.sync();
+    if (tot >= k) res = cand;
+  }
+  return res;
+}
+
+// k-th largest of n ordered float keys (f2key) in shared memory with ONE
+// histogram pass: 1024 bins linearly spaced between the min and max value
+// (monotone in the value), then the few members of the crossing bin are
+// ranked directly.  Falls back to the bitwise search when that bin is crowded
+// (ties / clustered values).  `hist` needs 1024 words, `mem` 64 words,
+// `tmp` 2*nwarps words, `res` 4 words.
+__device__ __forceinline__ uint32_t group_kth_largest_lin(const Group& g, const uint32_t* keys, int n, uint32_t k,
+                                                          uint32_t* hist, uint32_t* mem, uint32_t* tmp, int* res) {
+  constexpr int kNb = 1024, kMem = 64;
+  uint32_t mn = 0xFFFFFFFFu, mx = 0;
+  for (int i = g.tid; i < n; i += g.nthreads) {
+    mn = min(mn, keys[i]);
+    mx = max(mx, keys[i]);
+  }
+  for (int i = g.tid; i < kNb; i += g.nthreads) hist[i] = 0;
+  group_minmax_u32(g, mn, mx, tmp);
+  if (mn == mx) return mn;
+  const float vmin = key2f(mn), vmax = key2f(mx);
+  const float scale = (float)kNb / (vmax - vmin);
+  if (!(scale > 0.f) || isinf(scale)) return group_kth_largest_bs(g, keys, n, k, tmp);
+  auto bin = [&](uint32_t kk) {
+    const float x = (key2f(kk) - vmin) * scale;
+    return x >= (float)(kNb - 1) ? kNb - 1 : (int)x;
+  };
+  for (int i = g.tid; i < n; i += g.nthreads) atomicAdd(&hist[bin(keys[i])], 1u);
+  g.sync();
+  uint32_t above;
+  const int b = group_find_from_top(g, hist, kNb, k, tmp, res, above);
+  const int members = (int)hist[b];
+  if (members > kMem) return group_kth_largest_bs(g, keys, n, k, tmp);
+  if (g.tid == 0) res[2] = 0;
+  g.sync();
+  for (int i = g.tid; i < n; i += g.nthreads)
+    if (bin(keys[i]) == b) mem[atomicAdd(&res[2], 1)] = keys[i];
+  g.sync();
+  const uint32_t need = k - above;  // 1-based rank inside the bin
+  if (g.tid < members) {
+    const uint32_t x = mem[g.tid];
+    uint32_t gt = 0, ge = 0;
+    for (int j = 0; j < members; ++j) {
+      gt += mem[j] > x;
+      ge += mem[j] >= x;
+    }
+    if (gt < need && need <= ge) res[3] = (int)x;  // all writers agree
+  }
+  g.sync();
+  const uint32_t r = (uint32_t)res[3];
+  g.sync();
+  return r;
+}
+
 }  // namespace tw

@@ -17,6 +17,29 @@
 // ranked by (score desc, page asc).  The result is the reference's page set.
 #include "block_scan.cuh"
 
+#ifdef TW_TOPP_TRACE
+__device__ unsigned long long g_strace[512 * 16];
+__device__ int g_strace_phase[512];
+#define STRACE()                                                                                    \
+  do {                                                                                              \
+    if (threadIdx.x == 0 && blockIdx.x < 512) {                                                     \
+      unsigned long long now;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));                                      \
+      int ph = g_strace_phase[blockIdx.x]++;                                                        \
+      if (ph < 16) g_strace[blockIdx.x * 16 + ph] = now;                                            \
+    }                                                                                               \
+  } while (0)
+extern "C" int tw_debug_strace(unsigned long long* host_out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host_out, g_strace, sizeof(g_strace));
+  int zeros[512] = {0};
+  cudaMemcpyToSymbol(g_strace_phase, zeros, sizeof(zeros));
+  return 0;
+}
+#else
+#define STRACE() do {} while (0)
+#endif
+
 namespace tw {
 
 constexpr int kSelThreads = 512;
@@ -286,7 +309,8 @@ constexpr int kGroupThreads = kSelThreads / kSelGroups;
 
 struct SelGroupSmem {
   uint32_t tmp[2 * (kGroupThreads / 32)];
-  int res[2];
+  uint32_t mem[64];
+  int res[4];
   int namb, cin;
   float margin;
 };
@@ -319,6 +343,7 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
   double* terms = reinterpret_cast<double*>(smem + toff) + (threadIdx.x >> 5) * kHeadDim;  // [16 warps][128]
   SelGroupSmem& gs = GS[gp];
 
+  STRACE();
   for (int i = threadIdx.x; i < words; i += blockDim.x) ubits[i] = 0;
   const int k = min(P, prm.budget_pages);
   const int* pt = kv.page_table + (size_t)b * Pmax;
@@ -352,9 +377,12 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
         if (lane == 0) { gs.margin = qa * amax * (300.0f / 16777216.0f); gs.namb = 0; gs.cin = 0; }
       }
       for (int i = grp.tid; i < words; i += grp.nthreads) hbits[i] = 0;
+#pragma unroll 8
       for (int i = grp.tid; i < P; i += grp.nthreads) keys[i] = f2key(__ldcg(sc + i));
       grp.sync();
-      const float t = key2f(group_kth_largest(grp, keys, P, (uint32_t)k, hist, gs.tmp, gs.res));
+      STRACE();
+      const float t = key2f(group_kth_largest_lin(grp, keys, P, (uint32_t)k, hist, gs.mem, gs.tmp, gs.res));
+      STRACE();
       const float m2 = 2.f * gs.margin + 1e-6f * fabsf(t) + 1e-30f;
       const float hi_cut = t + m2, lo_cut = t - m2;
       for (int i = grp.tid; i < P; i += grp.nthreads) {
@@ -367,6 +395,7 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
         }
       }
       grp.sync();
+      STRACE();
       const int namb = gs.namb;
       const int need = k - gs.cin;
       if (grp.tid == 0) atomicAdd(&buf.counters[1], (uint32_t)namb);  // diagnostic: rescored pages
@@ -378,6 +407,7 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
         if (lane == 0) band_s[a] = s;
       }
       grp.sync();
+      STRACE();
       // rank inside the band: (score desc, page asc); keep the best `need`
       for (int a = grp.tid; a < namb; a += grp.nthreads) {
         const double sa = band_s[a];
@@ -398,6 +428,7 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
     }
   }
   __syncthreads();
+  STRACE();
   // compact the union bitmap -> ascending candidate page list
   int* out = buf.cand_pages + (size_t)unit * Pmax;
   uint32_t base = 0;
@@ -416,6 +447,7 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
     base += total;
   }
   if (threadIdx.x == 0) buf.cand_count[unit] = (int)base;
+  STRACE();
 }
 
 inline size_t select_smem_bytes(int Pmax) {

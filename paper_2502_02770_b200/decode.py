@@ -154,10 +154,19 @@ class DecodeStats:
     cand_pages: torch.Tensor  # union pages per unit
 
 
+def auto_chunk(cache: "PagedKVCache", sms: int = 148, warps_per_sm: int = 8) -> int:
+    """Attention work-item size: ~4 items per worker warp when half the
+    context survives, clamped to [64, 512] tokens (multiple of 16)."""
+    units = cache.num_seqs * cache.num_kv_heads
+    est = units * cache.max_pages * L.PAGE_SIZE * 0.5 / (4 * sms * warps_per_sm)
+    return 512 if est >= 384 else int(max(64, 16 * round(est / 16)))
+
+
 class DecodeBuffers:
     """Caller-owned intermediate buffers of one decode step (tw_decode_buffers)."""
 
-    def __init__(self, cache: PagedKVCache, chunk_tokens: int = L.DEFAULT_CHUNK, head_page_bits: bool = False):
+    def __init__(self, cache: PagedKVCache, chunk_tokens: int | None = None, head_page_bits: bool = False):
+        chunk_tokens = chunk_tokens or auto_chunk(cache)
         dev = cache.device
         U = cache.num_seqs * cache.num_kv_heads
         Hq = U * cache.group_size
@@ -208,8 +217,9 @@ class TwilightDecoder:
     """
 
     def __init__(self, cache: PagedKVCache, selector: str = "quest", budget=None, p: float = 0.95,
-                 chunk_tokens: int = L.DEFAULT_CHUNK, head_page_bits: bool = False,
+                 chunk_tokens: int | None = None, head_page_bits: bool = False,
                  bufs: DecodeBuffers | None = None):
+        chunk_tokens = chunk_tokens or auto_chunk(cache)
         if selector not in ("quest", "full"):
             raise ValueError(f"selector {selector!r} is not on the accelerated path (quest | full)")
         if not 0.0 <= p <= 1.0:

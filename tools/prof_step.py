@@ -51,6 +51,15 @@ if os.environ.get("TW_LIB_PATH"):
     print("phase durations us (mean over heads):", (d.mean(axis=0) / 1000).round(2).tolist())
     print("phase durations us (max):", (d.max(axis=0) / 1000).round(2).tolist())
     print("kernel span us:", (a[:, 6].max() - a[:, 0].min()) / 1000)
+    buf2 = (ctypes.c_ulonglong * (512 * 16))()
+    _lib.lib().tw_debug_strace(buf2)
+    s = np.frombuffer(buf2, dtype=np.uint64).reshape(512, 16).astype(np.int64)
+    units = cache.num_seqs * cache.num_kv_heads
+    s = s[:units]
+    nph = int((s > 0).sum(axis=1).max())
+    d = np.diff(s[:, :nph], axis=1)
+    print("select phases us (mean):", (d.mean(axis=0) / 1000).round(2).tolist())
+    print("select phases us (max):", (d.max(axis=0) / 1000).round(2).tolist())
 st = dec.stats()
 print("cand tokens/unit", float(st.cand_pages.float().mean()) * 16, "final/unit", float(st.group_b1.float().mean()),
       "rescored pages", int(dec.bufs.counters[1]))
