@@ -160,9 +160,9 @@ def algorithmic_bytes(cfg, dec, n, elem=2):
     units = B * H
     d = 128
     P = math.ceil(n / 16)
-    bufs = dec.bufs
-    U = bufs.cand_count.sum().item()  # candidate pages over all units
-    F = bufs.final_count.sum().item()  # surviving tokens over all units
+    bl = dec.bufs if isinstance(dec.bufs, list) else [dec.bufs]
+    U = sum(b.cand_count.sum().item() for b in bl)  # candidate pages over all units
+    F = sum(b.final_count.sum().item() for b in bl)  # surviving tokens over all units
     k1 = units * (2 * 2 * d * elem + d // 2 + 8 + 2 * 2 * d * elem)          # read k,v; write k,v,codes,params; meta RMW
     k2 = units * (P * 2 * d * elem + G * d * elem + 4 * P) if cfg["selector"] == "quest" else 0
     k3a = U * 1152                                                            # INT4 codes + fp32 scale/zero per page
@@ -199,7 +199,8 @@ def run_ours(args, cfg):
         batch = make_batch(B, H_local, G, n, dtype, tau=taus, seed=seed0 + layer, device=dev)
         cache.prefill(batch.K[:, :, : n - 1], batch.V[:, :, : n - 1])  # the step appends token n-1
         del batch
-        dec = TwilightDecoder(cache, cfg["selector"], budget=cfg["budget"], p=cfg["p"], bufs=shared)
+        dec = TwilightDecoder(cache, cfg["selector"], budget=cfg["budget"], p=cfg["p"], bufs=shared,
+                              waves=args.waves if B % max(args.waves, 1) == 0 else 1)
         shared = dec.bufs
         caches.append(cache)
         decs.append(dec)
@@ -264,8 +265,13 @@ def run_ours(args, cfg):
 
     # --- per-stage breakdown: each stage captured in its own CUDA graph, events between replays
     stage_names = ["K1_append", "K2_select", "K3a_estimate", "K3bc_topp", "K4_attention"]
-    stage_fns = lambda dec: [lambda: dec.cache.append(k_new, v_new, positions), lambda: dec.select(q),
-                             lambda: dec.estimate(q), lambda: dec.topp(), lambda: dec.attend(q, out)]
+    def stage_fns(dec):
+        subs = [(lo, hi, s) for lo, hi, s, _ in dec.waves] if dec.waves else [(0, B, dec)]
+        return [lambda: dec.cache.append(k_new, v_new, positions),
+                lambda: [s.select(q[lo:hi]) for lo, hi, s in subs],
+                lambda: [s.estimate(q[lo:hi]) for lo, hi, s in subs],
+                lambda: [s.topp() for lo, hi, s in subs],
+                lambda: [s.attend(q[lo:hi], out[lo:hi]) for lo, hi, s in subs]]
     stage_graphs = []
     for i in range(L):
         row = []
@@ -375,6 +381,7 @@ def run_ours(args, cfg):
         "dtype": "bf16",
         "data": "synthetic: K,V iid N(0,1) bf16, q N(0,1)/tau per KV head (tau cycles 0.25,0.5,1,2), seeded",
         "config": {"workload": cfg["desc"], "config_id": args.config, "batch_per_gpu": cfg["B"],
+                   "waves": len(decs[0].waves) or 1,
                    "global_batch": cfg["B"] * (world if cfg["shard"] == "batch" else 1), "ctx": n,
                    "kv_heads": H, "kv_heads_per_gpu": H_local, "group_size": G, "selector": cfg["selector"],
                    "budget_tokens": cfg["budget"], "p": cfg["p"],
@@ -535,6 +542,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--waves", type=int, default=1, help="sub-batches pipelined on separate streams (1 = off; measured slower at C2)")
     ap.add_argument("--cpu-units", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

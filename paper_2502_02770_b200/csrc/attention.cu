@@ -235,7 +235,8 @@ __global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const
   const int gw = blockIdx.x * kAttWarps + warp, nw = gridDim.x * kAttWarps;
   const int r = lane >> 2, t = lane & 3;
 
-  for (int it = gw; it < nitems_total; it += nw) {
+  uint32_t* ctr = buf.counters + (DENSE ? 5 : 4);
+  for (int it = warp_fetch(ctr); it < nitems_total; it = warp_fetch(ctr)) {
     const ItemDesc d = get_item<DENSE>(kv, buf, it, chunk, max_chunks);
     if (d.count <= 0) continue;
     const int b = d.unit / H, h = d.unit % H;
@@ -466,6 +467,7 @@ static int launch_attn(const tw_paged_kv* kv, const T* q, const tw_decode_buffer
   per_sm = per_sm < 1 ? 1 : per_sm;
   int grid = sms * per_sm;
   if (DENSE && grid * kAttWarps > total) grid = (total + kAttWarps - 1) / kAttWarps;
+  if (DENSE) cudaMemsetAsync(buf->counters + 5, 0, sizeof(uint32_t), s);  // dense runs without tw_select
   kern<<<grid, kAttThreads, smem, s>>>(*kv, q, *buf, out, chunk, max_chunks, total);
   merge_kernel<G, DENSE><<<units, 256, 0, s>>>(*kv, *buf, out, chunk, max_chunks);
   return launch_status();

@@ -175,6 +175,15 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Dynamic work distribution for persistent warp workers: lane 0 takes the
+// next item index from a global counter and broadcasts it (items are then
+// balanced even when CTAs start late, e.g. next to another stream's kernel).
+__device__ __forceinline__ int warp_fetch(uint32_t* ctr) {
+  int it = 0;
+  if ((threadIdx.x & 31) == 0) it = (int)atomicAdd(ctr, 1u);
+  return __shfl_sync(0xffffffffu, it, 0);
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }

@@ -94,7 +94,6 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
   __shared__ __align__(128) uint8_t ring[kEstWarps][kEstStages][kQBlockBytes];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane & 3, r = lane >> 2;
-  const int gw = blockIdx.x * kEstWarps + warp, nw = gridDim.x * kEstWarps;
   const int units = kv.num_seqs * kv.num_kv_heads;
   const int T_stride = kv.max_pages * kPage;
   const float inv_sqrt_d = 0.08838834764831845f;  // float32(1/sqrt(128)), as quantcache.py:258
@@ -115,7 +114,7 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       run_max[e] = -INFINITY;
     }
   };
-  for (int it = gw; it < units * max_chunks; it += nw) {
+  for (int it = warp_fetch(buf.counters + 3); it < units * max_chunks; it = warp_fetch(buf.counters + 3)) {
     const int unit = it % units;  // chunk-major: non-empty items come first, spread over all warps
     const int c0 = (it / units) * kEstPagesPerCta;
     const int ncand = buf.cand_count[unit];

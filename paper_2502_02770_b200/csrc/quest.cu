@@ -56,18 +56,18 @@ constexpr int kQfStages = 4;
 
 template <typename T, int G>
 __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_kernel(tw_paged_kv kv, const T* __restrict__ q,
-                                                                     float* __restrict__ scores, int max_chunks) {
+                                                                     float* __restrict__ scores, int max_chunks,
+                                                                     uint32_t* __restrict__ ctr) {
   __shared__ __align__(128) T ring[kQfWarps][kQfStages][2][2 * kHeadDim];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane & 15, half = lane >> 4;
-  const int gw = blockIdx.x * kQfWarps + warp, nw = gridDim.x * kQfWarps;
   const int units = kv.num_seqs * kv.num_kv_heads;
   constexpr int kPageBytes = 2 * kHeadDim * sizeof(T);
   constexpr int kChunks = kPageBytes / 16;  // 32 (bf16) or 64 (fp32) per page
   T (*R)[2][2 * kHeadDim] = ring[warp];
   float qr[G][8];
   int cur_unit = -1;
-  for (int it = gw; it < units * max_chunks; it += nw) {
+  for (int it = warp_fetch(ctr); it < units * max_chunks; it = warp_fetch(ctr)) {
     const int unit = it % units;
     const int p0 = (it / units) * kFilterPagesPerCta;
     const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
@@ -162,16 +162,16 @@ __device__ __forceinline__ void mma_bf16_q(float (&c)[4], const uint32_t (&a)[4]
 template <int G>
 __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_paged_kv kv,
                                                                          const __nv_bfloat16* __restrict__ q,
-                                                                         float* __restrict__ scores, int max_chunks) {
+                                                                         float* __restrict__ scores, int max_chunks,
+                                                                         uint32_t* __restrict__ ctr) {
   extern __shared__ __align__(128) uint8_t qm_ring[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane & 3, r = lane >> 2, q8 = lane >> 3, rr = lane & 7;
-  const int gw = blockIdx.x * kQfWarps + warp, nw = gridDim.x * kQfWarps;
   const int units = kv.num_seqs * kv.num_kv_heads;
   uint8_t (*R)[16 * 512] = reinterpret_cast<uint8_t (*)[16 * 512]>(qm_ring + (size_t)warp * kQmStages * 16 * 512);
   uint32_t qb[16][2];  // B fragments of [qneg ; qpos] for head column r
   int cur_unit = -1;
-  for (int it = gw; it < units * max_chunks; it += nw) {
+  for (int it = warp_fetch(ctr); it < units * max_chunks; it = warp_fetch(ctr)) {
     const int unit = it % units;
     const int p0 = (it / units) * kFilterPagesPerCta;
     const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
@@ -478,7 +478,7 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQfWarps * 32, 0);
       int grid = sms * (per_sm < 1 ? 1 : per_sm);
       if (grid * kQfWarps > items) grid = (items + kQfWarps - 1) / kQfWarps;
-      kern<<<grid, kQfWarps * 32, 0, stream>>>(*kv, qq, buf->page_scores, max_chunks);
+      kern<<<grid, kQfWarps * 32, 0, stream>>>(*kv, qq, buf->page_scores, max_chunks, buf->counters + 2);
     };
     if constexpr (sizeof(T) == 2) {
       auto gom = [&](auto kern) {
@@ -488,7 +488,8 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQfWarps * 32, smem);
         int grid = sms * (per_sm < 1 ? 1 : per_sm);
         if (grid * kQfWarps > items) grid = (items + kQfWarps - 1) / kQfWarps;
-        kern<<<grid, kQfWarps * 32, smem, stream>>>(*kv, (const __nv_bfloat16*)q, buf->page_scores, max_chunks);
+        kern<<<grid, kQfWarps * 32, smem, stream>>>(*kv, (const __nv_bfloat16*)q, buf->page_scores, max_chunks,
+                                                   buf->counters + 2);
       };
       switch (kv->group_size) {
         case 1: gom(quest_filter_mma_kernel<1>); break;

@@ -64,6 +64,18 @@ class PagedKVCache:
         self.seq_lens = torch.zeros(num_seqs, dtype=torch.int32, device=self.device)
         self._struct = None
 
+    def view(self, lo: int, hi: int) -> "PagedKVCache":
+        """Sequences [lo, hi) as a cache of their own, sharing the physical pool
+        (page table, lengths and |k| bounds are row slices)."""
+        v = PagedKVCache.__new__(PagedKVCache)
+        v.__dict__.update(self.__dict__)
+        v.num_seqs = hi - lo
+        v.page_table = self.page_table[lo:hi]
+        v.seq_lens = self.seq_lens[lo:hi]
+        v.kabsmax = self.kabsmax[lo:hi]
+        v._struct = None
+        return v
+
     # ------------------------------------------------------------------ ABI view
     def struct(self) -> L.TwPagedKV:
         if self._struct is None:
@@ -218,7 +230,22 @@ class TwilightDecoder:
 
     def __init__(self, cache: PagedKVCache, selector: str = "quest", budget=None, p: float = 0.95,
                  chunk_tokens: int | None = None, head_page_bits: bool = False,
-                 bufs: DecodeBuffers | None = None):
+                 bufs: DecodeBuffers | list | None = None, waves: int = 1):
+        self.waves = []
+        if waves > 1:
+            # sub-batches on their own streams: the select/top-p stages of one wave
+            # overlap the HBM-bound stages of another (see step()).
+            if cache.num_seqs % waves:
+                raise ValueError("num_seqs must divide into waves")
+            per = cache.num_seqs // waves
+            for w in range(waves):
+                sub = TwilightDecoder(cache.view(w * per, (w + 1) * per), selector, budget, p, chunk_tokens,
+                                      head_page_bits, bufs[w] if isinstance(bufs, list) else None)
+                self.waves.append((w * per, (w + 1) * per, sub, torch.cuda.Stream(device=cache.device)))
+            self.cache = cache
+            self.params = self.waves[0][2].params
+            self.bufs = [wv[2].bufs for wv in self.waves]
+            return
         chunk_tokens = chunk_tokens or auto_chunk(cache)
         if selector not in ("quest", "full"):
             raise ValueError(f"selector {selector!r} is not on the accelerated path (quest | full)")
@@ -272,6 +299,10 @@ class TwilightDecoder:
     def dense(self, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if out is None:
             out = self._out()
+        if self.waves:
+            for lo, hi, sub, _ in self.waves:
+                sub.dense(q[lo:hi], out[lo:hi])
+            return out
         kv, _, buf = self._args()
         L.check(L.lib().tw_dense_attention(kv, L.ptr(q), buf, L.ptr(out), L.stream_handle()),
                 "tw_dense_attention")
@@ -293,16 +324,48 @@ class TwilightDecoder:
         """Attend with the cache as is (no append): K2 -> K3 -> K4."""
         q = self.check_q(q)
         out = self._out() if out is None else out
+        if self.waves:
+            for lo, hi, sub, _ in self.waves:
+                sub.forward(q[lo:hi], out[lo:hi])
+            return out
         self.select(q)
         self.estimate(q)
         self.topp()
         return self.attend(q, out)
+
+    def _step_waves(self, q, k_new, v_new, positions, out):
+        """Append for the whole batch, then each wave's K2 -> K4 on its own
+        stream; wave w+1 starts once wave w's estimate is done, so its
+        HBM-bound select/estimate overlap wave w's top-p and attention."""
+        self.cache.append(k_new, v_new, positions)
+        cur = torch.cuda.current_stream()
+        prev = torch.cuda.Event()
+        prev.record(cur)
+        done = []
+        for lo, hi, sub, stream in self.waves:
+            stream.wait_event(prev)
+            with torch.cuda.stream(stream):
+                qs = q[lo:hi]
+                sub.select(qs)
+                sub.estimate(qs)
+                prev = torch.cuda.Event()
+                prev.record(stream)
+                sub.topp()
+                sub.attend(qs, out[lo:hi])
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                done.append(ev)
+        for ev in done:
+            cur.wait_event(ev)
+        return out
 
     def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
              positions: torch.Tensor | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
         """One decode step: append (K1) then K2 -> K4, one fused C-ABI call."""
         q = self.check_q(q)
         out = self._out() if out is None else out
+        if self.waves:
+            return self._step_waves(q, k_new, v_new, positions, out)
         kv, prm, buf = self._args()
         pos = self.cache.seq_lens if positions is None else positions
         L.check(L.lib().tw_decode_step(kv, L.ptr(q), L.ptr(k_new), L.ptr(v_new), L.ptr(pos), prm, buf,
@@ -310,6 +373,10 @@ class TwilightDecoder:
         return out
 
     def stats(self) -> DecodeStats:
+        if self.waves:
+            parts = [wv[2].stats() for wv in self.waves]
+            return DecodeStats(*[torch.cat([getattr(p, f) for p in parts]) for f in
+                                 ("b0", "b1", "candidate_mass", "threshold_weight", "group_b1", "cand_pages")])
         b = self.bufs
         return DecodeStats(b0=b.head_stats[:, 3].clone(), b1=b.head_stats[:, 0].clone(),
                            candidate_mass=b.head_stats[:, 1].clone(), threshold_weight=b.head_stats[:, 2].clone(),

@@ -262,3 +262,20 @@ def test_k2_filter_bounds_within_margin_at_32k(tau):
             assert err <= margin, (err, margin)
     rescored = int(dec.bufs.counters[1])
     assert rescored < 0.02 * B * H * G * cache.max_pages, rescored
+
+
+def test_wave_pipelined_step_matches_single_wave():
+    B, H, G, n = 4, 2, 4, 2000
+    dtype = torch.bfloat16
+    a, batch = _cache(B, H, G, n, dtype, [2000, 1500, 1999, 777], seed=17, tau=tau_schedule(H, (0.3, 1.0)))
+    c, _ = _cache(B, H, G, n, dtype, [2000, 1500, 1999, 777], seed=17, tau=tau_schedule(H, (0.3, 1.0)))
+    q = batch.q.contiguous()
+    d1 = TwilightDecoder(a, "quest", budget=512, p=0.95)
+    d2 = TwilightDecoder(c, "quest", budget=512, p=0.95, waves=2)
+    o1 = d1.step(q, batch.k_new, batch.v_new)
+    o2 = d2.step(q, batch.k_new, batch.v_new)
+    torch.cuda.synchronize()
+    assert a.seq_lens.tolist() == c.seq_lens.tolist()
+    torch.testing.assert_close(o2, o1, rtol=1e-5, atol=1e-6)
+    s1, s2 = d1.stats(), d2.stats()
+    assert torch.equal(s1.group_b1, s2.group_b1) and torch.equal(s1.cand_pages, s2.cand_pages)
