@@ -43,6 +43,10 @@ CONFIGS = {
     "C3": dict(desc="LongChat-7B MHA shape (32 heads, d=128), batch 8, ctx 128k, full selector + top-p p=0.9, "
                     "head-sharded", B=8, H=32, G=1, n=131072, selector="full", budget=None, p=0.9, layers=2,
                shard="head"),
+    "C4": dict(desc="Llama-3.1-8B all 32 layers decode step, global batch 64, ctx 64k, batch-sharded, random-init "
+                    "weights; layers 0-1 dense, others Quest n/4 + top-p p=0.95; all layers alias one physical KV "
+                    "cache", B=64, H=8, G=4, n=65536, selector="quest", budget=16384, p=0.95, layers=32,
+               shard="batch", model=True),
     "C5": dict(desc="Llama-3.1-8B shape, batch 32, ctx 128k, Quest n/4 + top-p (p sweep point 0.9), "
                     "focused vs diffuse heads", B=32, H=8, G=4, n=131072, selector="quest", budget=32768, p=0.9,
                layers=2, shard="batch"),
@@ -173,6 +177,46 @@ def algorithmic_bytes(cfg, dec, n, elem=2):
             "step": k1 + k2 + k3a + k3bc + k4, "K5_dense": dense, "cand_pages": U, "final_tokens": F}
 
 
+STAGE_NAMES = ["K1_append", "K2_select", "K3a_estimate", "K3bc_topp", "K4_attention"]
+
+
+def stage_breakdown(decs, q, k_new, v_new, positions, out, reps):
+    """Mean µs of each stage (K1..K4) per step: every stage captured in its own
+    CUDA graph, CUDA events between replays, rotating over `decs`."""
+    stream = torch.cuda.current_stream()
+    B = q.shape[0]
+
+    def stage_fns(dec):
+        subs = [(lo, hi, s) for lo, hi, s, _ in dec.waves] if dec.waves else [(0, B, dec)]
+        return [lambda: dec.cache.append(k_new, v_new, positions),
+                lambda: [s.select(q[lo:hi]) for lo, hi, s in subs],
+                lambda: [s.estimate(q[lo:hi]) for lo, hi, s in subs],
+                lambda: [s.topp() for lo, hi, s in subs],
+                lambda: [s.attend(q[lo:hi], out[lo:hi]) for lo, hi, s in subs]]
+    stage_graphs = []
+    for dec in decs:
+        row = []
+        for fn in stage_fns(dec):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            row.append(g)
+        stage_graphs.append(row)
+    stage_ms = {k: 0.0 for k in STAGE_NAMES}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(STAGE_NAMES) + 1)]
+    for i in range(reps + 1):
+        ev[0].record(stream)
+        for j, g in enumerate(stage_graphs[i % len(decs)]):
+            g.replay()
+            ev[j + 1].record(stream)
+        torch.cuda.synchronize()
+        if i == 0:
+            continue
+        for j, k in enumerate(STAGE_NAMES):
+            stage_ms[k] += ev[j].elapsed_time(ev[j + 1]) / reps
+    return stage_ms
+
+
 def run_ours(args, cfg):
     from paper_2502_02770_b200.decode import DecodeBuffers, PagedKVCache, TwilightDecoder, pages_for
     from paper_2502_02770_b200.workload import make_batch, tau_schedule
@@ -264,36 +308,7 @@ def run_ours(args, cfg):
     clocks = clk.summary()
 
     # --- per-stage breakdown: each stage captured in its own CUDA graph, events between replays
-    stage_names = ["K1_append", "K2_select", "K3a_estimate", "K3bc_topp", "K4_attention"]
-    def stage_fns(dec):
-        subs = [(lo, hi, s) for lo, hi, s, _ in dec.waves] if dec.waves else [(0, B, dec)]
-        return [lambda: dec.cache.append(k_new, v_new, positions),
-                lambda: [s.select(q[lo:hi]) for lo, hi, s in subs],
-                lambda: [s.estimate(q[lo:hi]) for lo, hi, s in subs],
-                lambda: [s.topp() for lo, hi, s in subs],
-                lambda: [s.attend(q[lo:hi], out[lo:hi]) for lo, hi, s in subs]]
-    stage_graphs = []
-    for i in range(L):
-        row = []
-        for fn in stage_fns(decs[i]):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                fn()
-            row.append(g)
-        stage_graphs.append(row)
-    stage_ms = {k: 0.0 for k in stage_names}
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stage_names) + 1)]
-    reps = max(3, min(args.steps, 10))
-    for i in range(reps + 1):
-        ev[0].record(stream)
-        for j, g in enumerate(stage_graphs[i % L]):
-            g.replay()
-            ev[j + 1].record(stream)
-        torch.cuda.synchronize()
-        if i == 0:
-            continue
-        for j, k in enumerate(stage_names):
-            stage_ms[k] += ev[j].elapsed_time(ev[j + 1]) / reps
+    stage_ms = stage_breakdown(decs, q, k_new, v_new, positions, out, reps=max(3, min(args.steps, 10)))
 
     # --- dense decode attention (K5) on the same caches: the speedup baseline
     dense_graphs = []
@@ -353,8 +368,8 @@ def run_ours(args, cfg):
     dec0 = decs[(args.steps - 1) % L]
     ab = algorithmic_bytes(cfg, dec0, n)
     peak, peak_src = load_peak()
-    kernel_gbs = {k: (ab[k] / (stage_ms[k] * 1e-3) / 1e9 if stage_ms[k] > 0 and ab[k] else None) for k in stage_names}
-    dominant = max(stage_names, key=lambda k: stage_ms[k])
+    kernel_gbs = {k: (ab[k] / (stage_ms[k] * 1e-3) / 1e9 if stage_ms[k] > 0 and ab[k] else None) for k in STAGE_NAMES}
+    dominant = max(STAGE_NAMES, key=lambda k: stage_ms[k])
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -402,7 +417,7 @@ def run_ours(args, cfg):
                           "frac": round(achieved_step / peak, 4)},
         "kernels_us": {k: round(v * 1e3, 2) for k, v in stage_ms.items()},
         "kernels_gbs": {k: (round(v, 1) if v else None) for k, v in kernel_gbs.items()},
-        "algorithmic_bytes": {k: ab[k] for k in stage_names},
+        "algorithmic_bytes": {k: ab[k] for k in STAGE_NAMES},
         "dense_us_per_layer": round(dense_ms * 1e3, 2),
         "dense_gbs": round(ab["K5_dense"] / (dense_ms * 1e-3) / 1e9, 1),
         "speedup_vs_dense": round(dense_ms / ms, 3),
@@ -414,6 +429,177 @@ def run_ours(args, cfg):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(cfg, n, samples=args.cpu_units)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_model(args, cfg):
+    """C4: the whole 32-layer Llama-3.1-8B decode step (model.py), global batch
+    sharded over ranks (strong scaling, no collective).  value = step / layers."""
+    from paper_2502_02770_b200.model import LlamaConfig, LlamaTwilightDecoder
+    from paper_2502_02770_b200.workload import make_batch, tau_schedule
+
+    rank, world, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local if world > 1 else 0)
+    assert cfg["B"] % world == 0, "global batch must divide over ranks"
+    B, H, G, n = cfg["B"] // world, cfg["H"], cfg["G"], cfg["n"]
+    cfg = dict(cfg, B=B, H_local=H)
+    L = args.layers or cfg["layers"]
+    mcfg = LlamaConfig()
+    model = LlamaTwilightDecoder(mcfg, batch=B, ctx=n, selector=cfg["selector"], budget=cfg["budget"], p=cfg["p"],
+                                 device=dev, seed=11 + rank, n_layers=L, q_taus=TAUS)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    tokens = torch.randint(0, mcfg.vocab, (B,), device=dev, generator=torch.Generator(device=dev).manual_seed(5 + rank))
+    next_tok = torch.empty(B, dtype=torch.int64, device=dev)
+
+    def step():
+        logits = model.step(tokens)
+        torch.argmax(logits, dim=-1, out=next_tok)
+
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(stream)
+    with torch.cuda.stream(s):
+        step()
+    stream.wait_stream(s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local if world > 1 else 0) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    clocks = clk.summary()
+
+    # e2e: tokens from pinned host, next tokens back to pinned host, every step
+    tok_h = tokens.cpu().pin_memory()
+    next_h = torch.empty(B, dtype=torch.int64).pin_memory()
+    for _ in range(args.warmup):
+        tokens.copy_(tok_h, non_blocking=True)
+        graph.replay()
+        next_h.copy_(next_tok, non_blocking=True)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0.record(stream)
+    for _ in range(args.steps):
+        tokens.copy_(tok_h, non_blocking=True)
+        graph.replay()
+        next_h.copy_(next_tok, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+
+    # breakdown: attention of one Twilight layer (its real q/k/v from an eager step) and one dense layer
+    tw_layer = next(i for i in range(L) if i not in mcfg.bypass_layers)
+    dec = model.decs[tw_layer]
+    rec = {}
+    model.step(tokens, record=rec)
+    q, k_new, v_new = rec[tw_layer]
+    positions = model.positions
+    out = torch.empty(B, H * G, 128, dtype=torch.float32, device=dev)
+    reps = max(3, min(args.steps, 10))
+    stage_ms = stage_breakdown([dec], q, k_new, v_new, positions, out, reps)
+    ab = algorithmic_bytes(cfg, dec, n)  # candidate pages / final sets of that layer's step
+    stats = dec.stats()
+    b1 = stats.b1.float()
+    dense_dec = model.decs[mcfg.bypass_layers[0]] if mcfg.bypass_layers else dec
+    g = torch.cuda.CUDAGraph()
+    dense_dec.dense(q, out)
+    with torch.cuda.graph(g):
+        dense_dec.dense(q, out)
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps):
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dense_ms = e0.elapsed_time(e1) / reps
+    n_tw = sum(1 for i in range(L) if i not in mcfg.bypass_layers)
+    n_dense = L - n_tw
+    attn_ms = sum(stage_ms.values()) * n_tw + dense_ms * n_dense
+    peak, peak_src = load_peak()
+    kernel_gbs = {k: (ab[k] / (stage_ms[k] * 1e-3) / 1e9 if stage_ms[k] > 0 and ab[k] else None) for k in STAGE_NAMES}
+    dominant = max(STAGE_NAMES, key=lambda k: stage_ms[k])
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(args.config, {}).get(dominant)
+        except Exception:
+            traffic = None
+    wbytes = model.weight_bytes()
+    step_bytes = wbytes + n_tw * ab["step"] + n_dense * ab["K5_dense"]
+    res = {
+        "metric": METRIC,
+        "value": round(ms * 1e3 / L, 2),
+        "unit": "us/layer",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic: random-init weights N(0,0.02) (q-projection columns rescaled so q ~ N(0,1/tau^2) per KV "
+                "head, tau cycling 0.25,0.5,1,2 as in C2), K,V iid N(0,1) bf16 prefill, seeded tokens",
+        "config": {"workload": cfg["desc"], "config_id": args.config, "model": "Llama-3.1-8B shape (random init)",
+                   "layers": L, "global_batch": cfg["B"] * world, "batch_per_gpu": B, "seq_len": n, "ctx": n,
+                   "selector": cfg["selector"], "budget_tokens": cfg["budget"], "p": cfg["p"],
+                   "bypass_layers": list(mcfg.bypass_layers), "parallelism": f"batch-sharded x{world}",
+                   "l2": f"weights {wbytes / 1e9:.1f} GB + KV {model.caches[0].k_cache.numel() * 4 / 1e9:.1f} GB "
+                         "streamed per step (>> 126 MB L2)", "cuda_graphs": True,
+                   "kv_aliasing": "all layers alias one physical paged cache (BASELINE.md §4)"},
+        "e2e": {"value": round(e2e_ms * 1e3 / L, 2), "unit": "us/layer", "h2d_bytes_per_step": B * 8,
+                "d2h_bytes_per_step": B * 8,
+                "path": "LlamaTwilightDecoder.step (captured) with token ids from pinned host, argmax ids to host"},
+        "gpu_launches": (8 * n_tw + 3 * n_dense) * args.steps,
+        "roofline": {"bound": "hbm", "kernel": dominant,
+                     "achieved": round(kernel_gbs[dominant], 1) if kernel_gbs[dominant] else None,
+                     "peak": peak, "unit": "GB/s",
+                     "frac": round(kernel_gbs[dominant] / peak, 4) if kernel_gbs[dominant] else None,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": ab[dominant]},
+        "step_roofline": {"algorithmic_bytes": step_bytes, "weights_bytes": wbytes,
+                          "achieved_gbs_per_gpu": round(step_bytes / (ms * 1e-3) / 1e9, 1),
+                          "frac": round(step_bytes / (ms * 1e-3) / 1e9 / peak, 4)},
+        "step_split_ms": {"attention_twilight_layers": round(sum(stage_ms.values()) * n_tw, 3),
+                          "attention_dense_layers": round(dense_ms * n_dense, 3),
+                          "gemm_norm_rope_other": round(ms - attn_ms, 3)},
+        "kernels_us": {k: round(v * 1e3, 2) for k, v in stage_ms.items()},
+        "kernels_gbs": {k: (round(v, 1) if v else None) for k, v in kernel_gbs.items()},
+        "dense_layer_attention_us": round(dense_ms * 1e3, 2),
+        "all_dense_step_estimate_ms": round(ms - sum(stage_ms.values()) * n_tw + dense_ms * n_tw, 3),
+        "budgets": {"cand_tokens_mean_per_unit": round(ab["cand_pages"] * 16 / (B * H), 1),
+                    "final_tokens_mean_per_unit": round(ab["final_tokens"] / (B * H), 1),
+                    "head_b1_min": int(b1.min().item()), "head_b1_max": int(b1.max().item()),
+                    "head_b1_mean": round(float(b1.mean().item()), 1)},
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(cfg, n, samples=max(2, args.cpu_units // 4))
+        cb["sample"] += "; attention of one Twilight layer only (the reference has no model / GEMM code)"
+        res["cpu_baseline"] = cb
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -510,7 +696,7 @@ def run_reference(args, cfg):
     n = cfg["n"]
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     H_local = cfg["H"] // world if cfg["shard"] == "head" else cfg["H"]
-    units = cfg["B"] * H_local * (world if cfg["shard"] == "batch" else 1)
+    units = cfg["B"] * H_local * (world if cfg["shard"] == "batch" and not cfg.get("model") else 1)
     ctx = mp.get_context("fork")
     with ctx.Pool(cores, initializer=_pool_init, initargs=(cfg, n, 4242)) as pool:
         for _ in range(args.warmup):
@@ -551,6 +737,8 @@ def main():
     cfg = dict(CONFIGS[args.config])
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif cfg.get("model"):
+        run_model(args, cfg)
     else:
         run_ours(args, cfg)
 

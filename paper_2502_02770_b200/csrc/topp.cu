@@ -20,6 +20,8 @@
 //
 // K3c: the group's final set is the union over its G heads (pipeline.py:347);
 // it is compacted in ascending token order and cut into attention work items.
+#include <cfloat>
+
 #include "block_scan.cuh"
 #ifdef TW_TOPP_TRACE
 #include <cstdio>
@@ -43,151 +45,211 @@ __device__ int g_trace_phase[512];
 #define TRACE(tag) do {} while (0)
 #endif
 
-constexpr int kTopThreads = 512;
+#ifndef TW_TOPP_THREADS
+#define TW_TOPP_THREADS 512
+#endif
+constexpr int kTopThreads = TW_TOPP_THREADS;
+#ifndef TW_TOPP_MINB
+#define TW_TOPP_MINB 2
+#endif
 constexpr int kBins = 4096;
-constexpr int kRankCap = 512;          // members ranked O(k^2) in shared memory
-constexpr float kBinPerLogit = 120.0f; // bins cover (max - z) in [0, 34.1)
+constexpr int kRankCap = 512;           // members ranked O(k^2) in shared memory
+constexpr float kBinPerLogit = 120.0f;  // bins cover (max - z) in [0, 34.1)
+constexpr int kNW = kTopThreads / 32;
+constexpr int kPer = kBins / kTopThreads;
+static_assert(kPer <= 8, "find_crossing's step table covers 8 bins per thread");
+// exp(-i/120), i = 0..7
+__device__ constexpr double kStepExp[8] = {1.0, 0.991701292638876, 0.9834714538216175, 0.9753099120283326,
+                                           0.9672161004820059, 0.9591894571091382, 0.951229424500714,
+                                           0.9433354498734922};
 
-__device__ __forceinline__ void atomic_add_u64_split(uint32_t* lo, uint32_t* hi, uint64_t v) {
-  const uint32_t vlo = (uint32_t)v, vhi = (uint32_t)(v >> 32);
-  const uint32_t old = atomicAdd(lo, vlo);
-  const uint32_t carry = (uint32_t)(old + vlo < old);
-  if (vhi + carry) atomicAdd(hi, vhi + carry);
+// Masses.  Bin b of (max - z) has top t_b = M - b/120 (float) and weight
+// w_b = exp(t_b - M) (fp64).  A member has e_i = exp(z_i - M) = w_b r_i with
+// r_i = exp(z_i - t_b) in (0.9917, 1]; it is summed as the u32 fixed-point
+// deficit u_i = rint((1 - r_i) 2^kq) (< 2^kq / 120), so
+//     bin mass = w_b (count - sum u / 2^kq).
+// Counts and deficits are plain u32 shared-memory adds (no 64-bit carries),
+// exact and order-independent => deterministic.  r_i comes from the SFU over
+// a 1/120-logit range (~2e-7 relative); w_b is fp64.  The deepest bin (34+
+// logits below the max, weights < 2e-15) takes whatever lands there.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
-// Fixed-point softmax mass of logit z under max m: round(e * 2^sh) with
-// e = 2^((z - m) log2 e) on the SFU (rel. error ~1e-6 for z - m >= -40; the
-// scale is a power of two so the float->u64 conversion adds no error).
-__device__ __forceinline__ uint64_t mass_fx(float z, float m, float fscale) {
-  const float e = exp2f((z - m) * 1.4426950408889634f);
-  return __float2ull_rn(e * fscale);
+// bin of z: floor((M - z) * 120), clamped to the last bin
+__device__ __forceinline__ int dbin(float z, float M120) {
+  return min(__float2int_rz(fmaf(-z, kBinPerLogit, M120)), kBins - 1);
 }
 
-__device__ __forceinline__ int dbin(float z, float m) {
-  const float d = (m - z) * kBinPerLogit;
-  return d >= (float)(kBins - 1) ? kBins - 1 : (int)d;
+// Largest float z with dbin(z) >= b (dbin is non-increasing in z), so bin b is
+// the float interval (bin_ceiling(b + 1), bin_ceiling(b)].
+__device__ __forceinline__ float bin_ceiling(int b, float M, float M120) {
+  if (b <= 0) return INFINITY;
+  if (b >= kBins) return -INFINITY;
+  float e = M - (float)b / kBinPerLogit;
+  for (int i = 0; i < 64 && dbin(e, M120) < b; ++i) e = nextafterf(e, -INFINITY);
+  for (int i = 0; i < 64; ++i) {
+    const float up = nextafterf(e, INFINITY);
+    if (dbin(up, M120) < b) break;
+    e = up;
+  }
+  return e;
 }
 
-// u64 inclusive block scan (one value per thread)
-__device__ __forceinline__ uint64_t block_incl_scan_u64(uint64_t v, uint64_t* tmp, uint64_t& total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  uint64_t x = v;
+__device__ __forceinline__ float bin_top(float M, int b) { return fmaf(-(float)b, 1.0f / kBinPerLogit, M); }
+
+__device__ __forceinline__ uint32_t deficit(float z, float M, int b, float uscale) {
+  const float r = ex2_approx((z - bin_top(M, b)) * 1.4426950408889634f);
+  return (uint32_t)__float2int_rn(fmaxf(fmaf(-r, uscale, uscale), 0.0f));
+}
+
+__device__ __forceinline__ double class_mass(double w, uint64_t cnt, uint64_t usum, double inv_uscale) {
+  return w * ((double)cnt - (double)usum * inv_uscale);
+}
+
+// CTA-wide inclusive scan with a compile-time warp count.
+template <typename T>
+__device__ __forceinline__ T cta_incl_scan(T v, T* tmp, T& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  T x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    T y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
   if (lane == 31) tmp[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    uint64_t s = lane < nw ? tmp[lane] : 0;
+    T s = lane < kNW ? tmp[lane] : T(0);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      uint64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      T y = __shfl_up_sync(0xffffffffu, s, o);
       if (lane >= o) s += y;
     }
-    if (lane < nw) tmp[lane] = s;
+    if (lane < kNW) tmp[lane] = s;
   }
   __syncthreads();
   if (wid > 0) x += tmp[wid - 1];
-  total = tmp[nw - 1];
+  total = tmp[kNW - 1];
   __syncthreads();
   return x;
 }
 
 struct TopSmem {
   uint32_t cnt[kBins];
-  uint32_t mlo[kBins];
-  uint32_t mhi[kBins];
+  uint32_t usum[kBins];
   uint32_t mkey[kRankCap];
-  uint64_t mmass[kRankCap];
-  uint64_t scan_tmp[32];
-  uint32_t tmp32[40];
+  uint32_t mu[kRankCap];
+  double dtmp[32];
+  uint32_t utmp[32];
   int nmem;
   uint32_t kmin, kmax;
   int bin;
-  uint64_t above_mass;
+  double above_mass;
   uint32_t above_cnt;
   uint32_t thr;
-  uint32_t sel_cnt;
-  uint64_t sel_mass;
+  uint32_t selc;
+  unsigned long long selu;
 };
 
-// Find the first bin in `order` (ascending index = descending logit when
-// `descending_index` is false) whose running mass reaches target.
-__device__ __forceinline__ void find_crossing(TopSmem& S, double target, uint64_t base_mass, bool top_is_high) {
-  const int per = kBins / kTopThreads;
-  // thread t owns `per` consecutive bins in priority order
-  uint64_t local = 0;
-  uint32_t lcnt = 0;
-  for (int i = 0; i < per; ++i) {
-    const int rank = threadIdx.x * per + i;
-    const int bb = top_is_high ? (kBins - 1 - rank) : rank;
-    local += ((uint64_t)S.mhi[bb] << 32) | S.mlo[bb];
-    lcnt += S.cnt[bb];
+// First bin in priority order whose running mass (from base_mass) reaches
+// the target.  Level 0 (wconst <= 0): bins of (max - z) weighted w_b,
+// priority = ascending b, target = p_eff * (total mass), returned as Z.
+// Deeper levels: key sub-bins of one parent bin, all weighted wconst,
+// priority = descending index (highest key first).  Also returns the count
+// of everything scanned in `count_total`.
+__device__ __forceinline__ double find_crossing(TopSmem& S, double target, double base_mass, float M, double wconst,
+                                                double inv_uscale, double p_eff, uint32_t& count_total) {
+  const bool level0 = !(wconst > 0.0);
+  double m[kPer];
+  uint32_t c[kPer];
+  double w0 = wconst;
+  float t0 = 0.f;
+  if (level0) {  // w_b for this thread's kPer consecutive bins: one exp, then exact small-step corrections
+    t0 = bin_top(M, threadIdx.x * kPer);
+    w0 = exp((double)t0 - (double)M);
   }
-  uint64_t total;
-  const uint64_t incl = block_incl_scan_u64(local, S.scan_tmp, total);
+  double local = 0.0;
+  uint32_t lcnt = 0;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int rank = threadIdx.x * kPer + i;
+    const int bb = level0 ? rank : (kBins - 1 - rank);
+    c[i] = S.cnt[bb];
+    double w = wconst;
+    if (level0) {
+      // exp(t_b - M) = w0 * exp(t_b - t0);  t_b - t0 = -i/120 + d (d ~ float rounding, tiny)
+      const double d = ((double)bin_top(M, bb) - (double)t0) + (double)i / (double)kBinPerLogit;
+      w = w0 * kStepExp[i] * (1.0 + d * (1.0 + 0.5 * d));
+    }
+    m[i] = c[i] ? class_mass(w, c[i], S.usum[bb], inv_uscale) : 0.0;
+    local += m[i];
+    lcnt += c[i];
+  }
+  double total;
+  const double incl = cta_incl_scan<double>(local, S.dtmp, total);
   uint32_t ctot;
-  const uint32_t cincl = block_incl_scan(lcnt, S.tmp32, ctot);
-  const uint64_t excl = incl - local;
-  const uint32_t cexcl = cincl - lcnt;
+  const uint32_t cincl = cta_incl_scan<uint32_t>(lcnt, S.utmp, ctot);
+  count_total = ctot;
+  if (level0) target = p_eff * total;
+  const double excl = incl - local;
   if (threadIdx.x == 0) S.bin = -1;
   __syncthreads();
-  if ((double)(base_mass + excl) < target && target <= (double)(base_mass + incl)) {
-    uint64_t run = excl;
-    uint32_t crun = cexcl;
-    for (int i = 0; i < per; ++i) {
-      const int rank = threadIdx.x * per + i;
-      const int bb = top_is_high ? (kBins - 1 - rank) : rank;
-      const uint64_t m = ((uint64_t)S.mhi[bb] << 32) | S.mlo[bb];
-      if ((double)(base_mass + run + m) >= target) {
-        S.bin = bb;
-        S.above_mass = base_mass + run;
+  if (base_mass + excl < target && target <= base_mass + incl) {
+    double run = base_mass + excl;
+    uint32_t crun = cincl - lcnt;
+    bool found = false;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      if (!found && c[i] && run + m[i] >= target) {
+        found = true;
+        S.bin = level0 ? threadIdx.x * kPer + i : kBins - 1 - (threadIdx.x * kPer + i);
+        S.above_mass = run;
         S.above_cnt = crun;
-        break;
       }
-      run += m;
-      crun += S.cnt[bb];
+      run += m[i];
+      crun += c[i];
     }
   }
   __syncthreads();
+  return total;
 }
 
-// Vectorised walk over a head's logits: 4 x float4 in flight per thread.
+// Vectorised walk over a head's logits: kUnroll float4 in flight per thread.
+#ifndef TW_TOPP_UNROLL
+#define TW_TOPP_UNROLL 4
+#endif
+constexpr int kUnroll = TW_TOPP_UNROLL;
 template <typename F>
 __device__ __forceinline__ void for_each_logit(const float* __restrict__ z, int npos, F&& f) {
   const float4* z4 = reinterpret_cast<const float4*>(z);
   const int n4 = npos >> 2;
-  for (int base = threadIdx.x; base < n4; base += blockDim.x * 4) {
-    float4 v[4];
+  for (int base = threadIdx.x; base < n4; base += kTopThreads * kUnroll) {
+    float4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = base + u * blockDim.x;
+    for (int u = 0; u < kUnroll; ++u) {
+      const int i = base + u * kTopThreads;
       v[u] = i < n4 ? __ldcg(z4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = base + u * blockDim.x;
-      if (i < n4) {
-        f(4 * i, v[u].x);
-        f(4 * i + 1, v[u].y);
-        f(4 * i + 2, v[u].z);
-        f(4 * i + 3, v[u].w);
-      }
+    for (int u = 0; u < kUnroll; ++u) {
+      f(v[u].x);
+      f(v[u].y);
+      f(v[u].z);
+      f(v[u].w);
     }
   }
 }
 
 // One CTA per query head; the last head of a unit to finish also forms the
 // group's final set (K3c) and reserves its attention work items.
-__global__ void __launch_bounds__(kTopThreads) topp_head_kernel(tw_paged_kv kv, tw_decode_params prm,
-                                                                tw_decode_buffers buf) {
+__global__ void __launch_bounds__(kTopThreads, TW_TOPP_MINB) topp_head_kernel(tw_paged_kv kv, tw_decode_params prm,
+                                                                               tw_decode_buffers buf) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TopSmem& S = *reinterpret_cast<TopSmem*>(smem_raw);
   __shared__ int s_last;
-  __shared__ uint32_t s_selc;
-  __shared__ unsigned long long s_selm;
   const int qh = blockIdx.x;
   const int G = kv.group_size;
   const int unit = qh / G;
@@ -195,43 +257,40 @@ __global__ void __launch_bounds__(kTopThreads) topp_head_kernel(tw_paged_kv kv, 
   const size_t T = (size_t)kv.max_pages * kPage;
   const float* z = buf.logits + (size_t)qh * T;
   const float M = key2f(buf.head_max[qh]);
+  const float M120 = M * kBinPerLogit;
   const double p_eff = fmin(prm.p, 1.0) - 1e-9;
   float* stats = buf.head_stats + (size_t)qh * 4;
   uint32_t thr = 0xFFFFFFFFu;  // selects nothing
   uint32_t b0 = 0;
-  uint64_t Z = 0;
-  float fscale = 1.f;
-  uint32_t sel_cnt = 0;        // |{z >= thr}|   (counted from the histograms, no extra pass)
-  uint64_t sel_mass = 0;       // its fixed-point mass
+  double Z = 0.0;
+  uint32_t sel_cnt = 0;        // |{z >= thr}|   (from the histograms, no extra pass)
+  double sel_mass = 0.0;       // its mass
+  // deficit scale: a bin's u32 sum holds up to 2^32 / (2^kq / 120) members
+  const float uscale = npos > 120000 ? 1048576.0f : 4194304.0f;
+  const double inv_uscale = 1.0 / (double)uscale;
   const bool empty = p_eff <= 0.0 || npos == 0 || !(M > -INFINITY);
   TRACE("start");
   if (!empty) {
-    // fixed-point scale: sums of up to npos terms stay below 2^63
-    const int lg = 32 - __clz(npos);
-    fscale = ldexpf(1.f, 62 - lg);
-    for (int i = threadIdx.x; i < kBins; i += blockDim.x) { S.cnt[i] = 0; S.mlo[i] = 0; S.mhi[i] = 0; }
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      S.cnt[threadIdx.x + i * kTopThreads] = 0;
+      S.usum[threadIdx.x + i * kTopThreads] = 0;
+    }
     __syncthreads();
-    uint64_t zt = 0;
-    uint32_t nvalid = 0;
-    for_each_logit(z, npos, [&](int, float zi) {
-      if (zi == -INFINITY) return;
-      ++nvalid;
-      const uint64_t mf = mass_fx(zi, M, fscale);
-      const int bb = dbin(zi, M);
-      atomicAdd(&S.cnt[bb], 1u);
-      if (mf) atomic_add_u64_split(&S.mlo[bb], &S.mhi[bb], mf);
-      zt += mf;
+    for_each_logit(z, npos, [&](float zi) {
+      if (zi > -INFINITY) {
+        const int bb = dbin(zi, M120);
+        atomicAdd(&S.cnt[bb], 1u);
+        atomicAdd(&S.usum[bb], deficit(zi, M, bb, uscale));
+      }
     });
+    __syncthreads();
     TRACE("pass1");
-    block_incl_scan_u64(zt, S.scan_tmp, Z);
-    block_incl_scan(nvalid, S.tmp32, b0);
-    const double target = p_eff * (double)Z;
-
-    // level 0: bins of (max - z), highest logit first (= ascending bin index)
-    find_crossing(S, target, 0, false);
+    Z = find_crossing(S, 0.0, 0.0, M, 0.0, inv_uscale, p_eff, b0);
+    const double target = p_eff * Z;
     TRACE("crossing");
     int bin = S.bin;
-    uint64_t above_mass = S.above_mass;
+    double above_mass = S.above_mass;
     uint32_t above_cnt = S.above_cnt;
     uint32_t klo = 0, khi = 0xFFFFFFFFu;
     bool resolved = false;
@@ -241,22 +300,33 @@ __global__ void __launch_bounds__(kTopThreads) topp_head_kernel(tw_paged_kv kv, 
       sel_mass = Z;
       resolved = true;
     }
+    const int pbin = bin;  // parent bin of every deeper level
+    __shared__ float s_zr[2];
+    if (!resolved && threadIdx.x == 0) {
+      s_zr[0] = bin_ceiling(pbin + 1, M, M120);  // members: zlo < z <= zhi
+      s_zr[1] = bin_ceiling(pbin, M, M120);
+    }
+    __syncthreads();
+    const float zlo = s_zr[0], zhi = s_zr[1];
+    const double wb = resolved ? 0.0 : exp((double)bin_top(M, pbin) - (double)M);
     int members = resolved ? 0 : (int)S.cnt[bin];
-    uint64_t range_mass = resolved ? 0 : (((uint64_t)S.mhi[bin] << 32) | S.mlo[bin]);
+    double range_mass = resolved ? 0.0 : class_mass(wb, S.cnt[bin], S.usum[bin], inv_uscale);
     while (!resolved) {
       __syncthreads();
       if (members <= kRankCap) {
         // compact the members, then rank them exactly
-        if (threadIdx.x == 0) { S.nmem = 0; s_selc = 0; s_selm = 0; }
+        if (threadIdx.x == 0) { S.nmem = 0; S.selc = 0; S.selu = 0; }
         __syncthreads();
-        for_each_logit(z, npos, [&](int, float zi) {
-          if (zi == -INFINITY || dbin(zi, M) != bin) return;
-          const uint32_t k = f2key(zi);
-          if (k < klo || k > khi) return;
-          const int slot = atomicAdd(&S.nmem, 1);
-          if (slot < kRankCap) {
-            S.mkey[slot] = k;
-            S.mmass[slot] = mass_fx(zi, M, fscale);
+        for_each_logit(z, npos, [&](float zi) {
+          if (zi > zlo && zi <= zhi) {
+            const uint32_t k = f2key(zi);
+            if (k >= klo && k <= khi) {
+              const int slot = atomicAdd(&S.nmem, 1);
+              if (slot < kRankCap) {
+                S.mkey[slot] = k;
+                S.mu[slot] = deficit(zi, M, pbin, uscale);
+              }
+            }
           }
         });
         __syncthreads();
@@ -264,41 +334,51 @@ __global__ void __launch_bounds__(kTopThreads) topp_head_kernel(tw_paged_kv kv, 
         const int nm = min(S.nmem, kRankCap);
         if (threadIdx.x == 0) S.thr = klo;  // fallback (rounding): keep the whole range
         __syncthreads();
-        for (int a = threadIdx.x; a < nm; a += blockDim.x) {
+        for (int a = threadIdx.x; a < nm; a += kTopThreads) {
           const uint32_t ka = S.mkey[a];
-          uint64_t above = 0, eq = 0;
+          uint32_t cgt = 0, ceq = 0;
+          uint64_t ugt = 0, ueq = 0;
           for (int j = 0; j < nm; ++j) {
             const uint32_t kj = S.mkey[j];
-            const uint64_t mj = S.mmass[j];
-            above += kj > ka ? mj : 0;
-            eq += kj == ka ? mj : 0;
+            const uint32_t uj = S.mu[j];
+            cgt += kj > ka;
+            ugt += kj > ka ? uj : 0u;
+            ceq += kj == ka;
+            ueq += kj == ka ? uj : 0u;
           }
-          if ((double)(above_mass + above) < target && target <= (double)(above_mass + above + eq))
-            S.thr = ka;  // every writer of this class writes the same key
+          const double lo = above_mass + class_mass(wb, cgt, ugt, inv_uscale);
+          const double hi = lo + class_mass(wb, ceq, ueq, inv_uscale);
+          if (lo < target && target <= hi) S.thr = ka;  // every writer of this class writes the same key
         }
         __syncthreads();
         thr = S.thr;
-        for (int a = threadIdx.x; a < nm; a += blockDim.x)
+        for (int a = threadIdx.x; a < nm; a += kTopThreads)
           if (S.mkey[a] >= thr) {
-            atomicAdd(&s_selc, 1u);
-            atomicAdd(&s_selm, (unsigned long long)S.mmass[a]);
+            atomicAdd(&S.selc, 1u);
+            atomicAdd(&S.selu, (unsigned long long)S.mu[a]);
           }
         __syncthreads();
         TRACE("ranked");
-        sel_cnt = above_cnt + s_selc;
-        sel_mass = above_mass + s_selm;
+        sel_cnt = above_cnt + S.selc;
+        sel_mass = above_mass + class_mass(wb, S.selc, S.selu, inv_uscale);
         resolved = true;
       } else {
-        // split the range by key: min/max key of the members, 4096 key bins
+        // split the range by key: min/max key of the members, 4096 key sub-bins
         if (threadIdx.x == 0) { S.kmin = 0xFFFFFFFFu; S.kmax = 0; }
-        for (int i = threadIdx.x; i < kBins; i += blockDim.x) { S.cnt[i] = 0; S.mlo[i] = 0; S.mhi[i] = 0; }
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          S.cnt[threadIdx.x + i * kTopThreads] = 0;
+          S.usum[threadIdx.x + i * kTopThreads] = 0;
+        }
         __syncthreads();
-        for_each_logit(z, npos, [&](int, float zi) {
-          if (zi == -INFINITY || dbin(zi, M) != bin) return;
-          const uint32_t k = f2key(zi);
-          if (k < klo || k > khi) return;
-          atomicMin(&S.kmin, k);
-          atomicMax(&S.kmax, k);
+        for_each_logit(z, npos, [&](float zi) {
+          if (zi > zlo && zi <= zhi) {
+            const uint32_t k = f2key(zi);
+            if (k >= klo && k <= khi) {
+              atomicMin(&S.kmin, k);
+              atomicMax(&S.kmax, k);
+            }
+          }
         });
         __syncthreads();
         const uint32_t kmin = S.kmin, kmax = S.kmax;
@@ -309,17 +389,19 @@ __global__ void __launch_bounds__(kTopThreads) topp_head_kernel(tw_paged_kv kv, 
           break;
         }
         const int sh = max(0, (32 - __clz(kmax - kmin)) - 12);
-        for_each_logit(z, npos, [&](int, float zi) {
-          if (zi == -INFINITY || dbin(zi, M) != bin) return;
-          const uint32_t k = f2key(zi);
-          if (k < klo || k > khi) return;
-          const int sb = (int)((k - kmin) >> sh);
-          atomicAdd(&S.cnt[sb], 1u);
-          const uint64_t mf = mass_fx(zi, M, fscale);
-          if (mf) atomic_add_u64_split(&S.mlo[sb], &S.mhi[sb], mf);
+        for_each_logit(z, npos, [&](float zi) {
+          if (zi > zlo && zi <= zhi) {
+            const uint32_t k = f2key(zi);
+            if (k >= klo && k <= khi) {
+              const int sb = (int)((k - kmin) >> sh);
+              atomicAdd(&S.cnt[sb], 1u);
+              atomicAdd(&S.usum[sb], deficit(zi, M, pbin, uscale));
+            }
+          }
         });
         __syncthreads();
-        find_crossing(S, target, above_mass, true);  // highest key first
+        uint32_t dummy;
+        find_crossing(S, target, above_mass, M, wb, inv_uscale, p_eff, dummy);  // highest key first
         if (S.bin < 0) {
           thr = kmin;
           sel_cnt = above_cnt + members;
@@ -330,7 +412,7 @@ __global__ void __launch_bounds__(kTopThreads) topp_head_kernel(tw_paged_kv kv, 
         above_mass = S.above_mass;
         above_cnt += S.above_cnt;
         members = (int)S.cnt[sb];
-        range_mass = ((uint64_t)S.mhi[sb] << 32) | S.mlo[sb];
+        range_mass = class_mass(wb, S.cnt[sb], S.usum[sb], inv_uscale);
         klo = kmin + ((uint32_t)sb << sh);
         khi = min(kmax, klo + ((1u << sh) - 1u));
       }
@@ -338,32 +420,38 @@ __global__ void __launch_bounds__(kTopThreads) topp_head_kernel(tw_paged_kv kv, 
     __syncthreads();
   }
   TRACE("resolved");
-  // selection bitmap of the head's pruned set {z >= thr} (key compares only)
+  // selection bitmap of the head's pruned set {z >= z_thr} (float compares; -inf never selected)
   uint32_t* bits = buf.sel_bits + (size_t)qh * (T / 32);
   {
+    const float zthr = thr == 0u ? -FLT_MAX : key2f(thr);  // thr = ~0 -> NaN: selects nothing
     const float4* z4 = reinterpret_cast<const float4*>(z);
     const int n4 = npos >> 2;
     const int lane = threadIdx.x & 31;
-    for (int i0 = 0; i0 < n4; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      uint32_t nib = 0;
-      if (i < n4) {
-        const float4 v = __ldcg(z4 + i);
-        nib = (v.x != -INFINITY && f2key(v.x) >= thr ? 1u : 0u) | (v.y != -INFINITY && f2key(v.y) >= thr ? 2u : 0u) |
-              (v.z != -INFINITY && f2key(v.z) >= thr ? 4u : 0u) | (v.w != -INFINITY && f2key(v.w) >= thr ? 8u : 0u);
+    for (int i0 = 0; i0 < n4; i0 += kTopThreads * kUnroll) {
+      float4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int i = i0 + u * kTopThreads + threadIdx.x;
+        v[u] = i < n4 ? __ldcg(z4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       }
-      uint32_t w = nib << (4 * (lane & 7));
-      w |= __shfl_xor_sync(0xffffffffu, w, 1);
-      w |= __shfl_xor_sync(0xffffffffu, w, 2);
-      w |= __shfl_xor_sync(0xffffffffu, w, 4);
-      if ((lane & 7) == 0 && i < n4) bits[i >> 3] = w;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int i = i0 + u * kTopThreads + threadIdx.x;
+        const uint32_t nib = (v[u].x >= zthr ? 1u : 0u) | (v[u].y >= zthr ? 2u : 0u) | (v[u].z >= zthr ? 4u : 0u) |
+                             (v[u].w >= zthr ? 8u : 0u);
+        uint32_t w = nib << (4 * (lane & 7));
+        w |= __shfl_xor_sync(0xffffffffu, w, 1);
+        w |= __shfl_xor_sync(0xffffffffu, w, 2);
+        w |= __shfl_xor_sync(0xffffffffu, w, 4);
+        if ((lane & 7) == 0 && i < n4) bits[i >> 3] = w;
+      }
     }
   }
   if (threadIdx.x == 0) {
     buf.head_thr[qh] = thr;
     stats[0] = (float)sel_cnt;
-    stats[1] = empty ? 0.f : (float)((double)sel_mass / (double)Z);
-    stats[2] = empty ? 0.f : (float)((double)mass_fx(key2f(thr), M, fscale) / (double)Z);
+    stats[1] = empty ? 0.f : (float)(sel_mass / Z);
+    stats[2] = empty ? 0.f : (float)(exp((double)key2f(thr) - (double)M) / Z);
     stats[3] = (float)b0;
   }
   TRACE("bitmap");
@@ -379,19 +467,21 @@ __global__ void __launch_bounds__(kTopThreads) topp_head_kernel(tw_paged_kv kv, 
   const int words = (npos + 31) >> 5;
   const uint32_t* hb = buf.sel_bits + (size_t)unit * G * (T / 32);
   uint32_t base = 0;
-  for (int w0 = 0; w0 < words; w0 += blockDim.x) {
+  for (int w0 = 0; w0 < words; w0 += kTopThreads) {
     const int w = w0 + threadIdx.x;
     uint32_t x = 0;
     if (w < words)
       for (int g = 0; g < G; ++g) x |= __ldcg(hb + (size_t)g * (T / 32) + w);
+    // a word covers candidate pages 2w and 2w+1: fetch both page ids before the scan
+    const int c0 = x & 0xFFFFu ? cand[2 * w] * kPage : 0;
+    const int c1 = x >> 16 ? cand[2 * w + 1] * kPage - 16 : 0;
     uint32_t total;
-    const uint32_t incl = block_incl_scan(__popc(x), S.tmp32, total);
+    const uint32_t incl = cta_incl_scan<uint32_t>(__popc(x), S.utmp, total);
     uint32_t pos = base + incl - __popc(x);
     while (x) {
       const int bit = __ffs(x) - 1;
       x &= x - 1;
-      const int pp = w * 32 + bit;
-      out[pos++] = cand[pp >> 4] * kPage + (pp & 15);
+      out[pos++] = (bit < 16 ? c0 : c1) + bit;
     }
     base += total;
   }
