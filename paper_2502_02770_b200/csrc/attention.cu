@@ -464,8 +464,7 @@ static int launch_attn(const tw_paged_kv* kv, const T* q, const tw_decode_buffer
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAttThreads, smem);
-  per_sm = per_sm < 1 ? 1 : per_sm;
-  int grid = sms * per_sm;
+  int grid = sms * persist_cap(per_sm);
   if (DENSE && grid * kAttWarps > total) grid = (total + kAttWarps - 1) / kAttWarps;
   if (DENSE) cudaMemsetAsync(buf->counters + 5, 0, sizeof(uint32_t), s);  // dense runs without tw_select
   kern<<<grid, kAttThreads, smem, s>>>(*kv, q, *buf, out, chunk, max_chunks, total);

@@ -1,5 +1,6 @@
 // Shared device helpers for the Twilight sm_100a kernels.
 #pragma once
+#include <cstdlib>
 
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -186,6 +187,18 @@ __device__ __forceinline__ int warp_fetch(uint32_t* ctr) {
 
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Experiment knob: cap the resident CTAs per SM of the persistent kernels
+// (TW_PERSIST_CTAS=n; unset = as many as fit).
+inline int persist_cap(int per_sm) {
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("TW_PERSIST_CTAS");
+    cap = e ? atoi(e) : 0;
+  }
+  if (per_sm < 1) per_sm = 1;
+  return cap > 0 && cap < per_sm ? cap : per_sm;
 }
 
 }  // namespace tw

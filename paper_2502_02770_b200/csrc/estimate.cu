@@ -38,6 +38,38 @@ __device__ __forceinline__ void mma_u8s8(int (&c)[4], const uint32_t (&a)[4], ui
 constexpr int kDigits = 3;         // q as 3 signed base-256 digits of a 22-bit fixed-point value
 constexpr int kEstStages = 4;      // pages in flight per warp (cp.async ring)
 
+// vector loads of 4 / 32 consecutive q elements as float
+__device__ __forceinline__ void load4(const __nv_bfloat16* p, float& a, float& b, float& c, float& d) {
+  const uint2 w = __ldg(reinterpret_cast<const uint2*>(p));
+  a = __uint_as_float(w.x << 16); b = __uint_as_float(w.x & 0xFFFF0000u);
+  c = __uint_as_float(w.y << 16); d = __uint_as_float(w.y & 0xFFFF0000u);
+}
+__device__ __forceinline__ void load4(const float* p, float& a, float& b, float& c, float& d) {
+  const float4 w = __ldg(reinterpret_cast<const float4*>(p));
+  a = w.x; b = w.y; c = w.z; d = w.w;
+}
+__device__ __forceinline__ void load32(const __nv_bfloat16* p, float (&v)[32]) {
+  uint4 w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) w[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t x[4] = {w[i].x, w[i].y, w[i].z, w[i].w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[8 * i + 2 * k] = __uint_as_float(x[k] << 16);
+      v[8 * i + 2 * k + 1] = __uint_as_float(x[k] & 0xFFFF0000u);
+    }
+  }
+}
+__device__ __forceinline__ void load32(const float* p, float (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float4 w = __ldg(reinterpret_cast<const float4*>(p) + i);
+    v[4 * i] = w.x; v[4 * i + 1] = w.y; v[4 * i + 2] = w.z; v[4 * i + 3] = w.w;
+  }
+}
+
 // q fixed point + digit B fragments for the lane's B column (head r), and for
 // the lane's two accumulator columns (heads 2t, 2t+1): sum(q) and 2^-S.
 template <typename T, int G>
@@ -50,19 +82,22 @@ __device__ __forceinline__ void estimate_prologue(const T* __restrict__ q, int u
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const T* qg = q + ((size_t)unit * G + g) * kHeadDim + 4 * lane;
-    const float v0 = Elem<T>::to_f(qg[0]), v1 = Elem<T>::to_f(qg[1]), v2 = Elem<T>::to_f(qg[2]),
-                v3 = Elem<T>::to_f(qg[3]);
+    float v0, v1, v2, v3;
+    load4(qg, v0, v1, v2, v3);
     float s = (v0 + v1) + (v2 + v3);
     float m = fmaxf(fmaxf(fabsf(v0), fabsf(v1)), fmaxf(fabsf(v2), fabsf(v3)));
     s = warp_sum(s);
     m = warp_max(m);
-    const int S = m > 0.f ? 21 - ilogbf(m) : 0;
+    const int S = m > 0.f ? min(21 - ilogbf(m), 126) : 0;
     if (g == r) my_maxabs = (float)S;
     if (g == 2 * t) { sq[0] = s; inv_scale[0] = ldexpf(1.f, -S); }
     if (g == 2 * t + 1) { sq[1] = s; inv_scale[1] = ldexpf(1.f, -S); }
   }
   const int S = (int)my_maxabs;
-  const T* qh = q + ((size_t)unit * G + (r < G ? r : 0)) * kHeadDim;
+  // the lane's channels 32t .. 32t+31 of head r (one contiguous 64/128-B run)
+  float qv[32];
+  load32(q + ((size_t)unit * G + (r < G ? r : 0)) * kHeadDim + 32 * t, qv);
+  const float qscale = ldexpf(1.f, S);  // exact power of two
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
 #pragma unroll
@@ -71,8 +106,7 @@ __device__ __forceinline__ void estimate_prologue(const T* __restrict__ q, int u
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         // k-slot 4t+i (+16 for half 1) <-> channel 32t + 8j + 2i (+1)
-        const int ch = 32 * t + 8 * j + 2 * i + half;
-        int x = r < G ? __float2int_rn(ldexpf(Elem<T>::to_f(qh[ch]), S)) : 0;
+        int x = r < G ? __float2int_rn(qv[8 * j + 2 * i + half] * qscale) : 0;
 #pragma unroll
         for (int k = 0; k < kDigits; ++k) {
           const int d = k + 1 < kDigits ? ((x + 128) & 255) - 128 : x;  // balanced digit, last takes the rest
@@ -246,7 +280,7 @@ static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, estimate_kernel<T, G>, kEstWarps * 32, 0);
   const int items = kv->num_seqs * kv->num_kv_heads * max_chunks;
-  int grid = sms * (per_sm < 1 ? 1 : per_sm);
+  int grid = sms * persist_cap(per_sm);
   if (grid * kEstWarps > items) grid = (items + kEstWarps - 1) / kEstWarps;
   estimate_kernel<T, G><<<grid, kEstWarps * 32, 0, stream>>>(*kv, q, *buf, max_chunks);
 }

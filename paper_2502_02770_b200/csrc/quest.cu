@@ -204,20 +204,24 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
       cp_commit();
     }
     if (unit != cur_unit) {
-      const __nv_bfloat16* qh = q + ((size_t)unit * G + (r < G ? r : 0)) * kHeadDim;
+      // k = 16kk + {2t, 2t+1 | 2t+8, 2t+9}; k < 128 -> qneg[k], else qpos[k - 128]:
+      // the bf16 pair (c, c+1), c = k & 127, is 32-bit word 8(kk & 7) + t + 4hb of the head's row
+      const uint32_t* qw = reinterpret_cast<const uint32_t*>(q + ((size_t)unit * G + (r < G ? r : 0)) * kHeadDim);
+      uint32_t w[8][2];
 #pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        // k = 16kk + {2t, 2t+1 | 2t+8, 2t+9}; k < 128 -> qneg[k], else qpos[k - 128]
+      for (int k8 = 0; k8 < 8; ++k8) {
+        w[k8][0] = r < G ? __ldg(qw + 8 * k8 + t) : 0u;
+        w[k8][1] = r < G ? __ldg(qw + 8 * k8 + t + 4) : 0u;
+      }
+      const __nv_bfloat162 zero2 = __float2bfloat162_rn(0.f);
+#pragma unroll
+      for (int k8 = 0; k8 < 8; ++k8) {
 #pragma unroll
         for (int hb = 0; hb < 2; ++hb) {
-          const int k0 = 16 * kk + 2 * t + 8 * hb;
-          const int c = k0 & 127;
-          float a = r < G ? __bfloat162float(qh[c]) : 0.f;
-          float bq = r < G ? __bfloat162float(qh[c + 1]) : 0.f;
-          if (kk < 8) { a = fminf(a, 0.f); bq = fminf(bq, 0.f); }
-          else { a = fmaxf(a, 0.f); bq = fmaxf(bq, 0.f); }
-          __nv_bfloat162 v = __floats2bfloat162_rn(a, bq);
-          qb[kk][hb] = *reinterpret_cast<uint32_t*>(&v);
+          const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&w[k8][hb]);
+          const __nv_bfloat162 neg = __hmin2(v, zero2), pos = __hmax2(v, zero2);
+          qb[k8][hb] = *reinterpret_cast<const uint32_t*>(&neg);
+          qb[k8 + 8][hb] = *reinterpret_cast<const uint32_t*>(&pos);
         }
       }
       cur_unit = unit;
@@ -476,7 +480,7 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
     auto go = [&](auto kern) {
       int per_sm = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQfWarps * 32, 0);
-      int grid = sms * (per_sm < 1 ? 1 : per_sm);
+      int grid = sms * persist_cap(per_sm);
       if (grid * kQfWarps > items) grid = (items + kQfWarps - 1) / kQfWarps;
       kern<<<grid, kQfWarps * 32, 0, stream>>>(*kv, qq, buf->page_scores, max_chunks, buf->counters + 2);
     };
@@ -486,7 +490,7 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQfWarps * 32, smem);
-        int grid = sms * (per_sm < 1 ? 1 : per_sm);
+        int grid = sms * persist_cap(per_sm);
         if (grid * kQfWarps > items) grid = (items + kQfWarps - 1) / kQfWarps;
         kern<<<grid, kQfWarps * 32, smem, stream>>>(*kv, (const __nv_bfloat16*)q, buf->page_scores, max_chunks,
                                                    buf->counters + 2);

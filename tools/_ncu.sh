@@ -1,3 +1,2 @@
-ncu --set full --import-source on --clock-control none -k regex:topp_head -c 1 -o gpurun_out/topp_old -f env TW_LIB_PATH=tools/_variants/minb2/libtwilight.so python tools/prof_step.py --config C2 --reps 1 > /dev/null 2>&1
-ncu --set full --import-source on --clock-control none -k regex:topp_head -c 1 -o gpurun_out/topp_new -f env TW_LIB_PATH=tools/_variants/new_m2/libtwilight.so python tools/prof_step.py --config C2 --reps 1 > /dev/null 2>&1
-ls -la gpurun_out/*.ncu-rep
+ncu --set full --import-source on --clock-control none -k regex:'append_kernel|quest_filter|quest_select|estimate_kernel|topp_head|attn_kernel|merge_kernel' -c 8 -o gpurun_out/step_c2 -f python tools/prof_step.py --config C2 --reps 1 > gpurun_out/ncu_step.log 2>&1
+ls -la gpurun_out/step_c2.ncu-rep

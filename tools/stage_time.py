@@ -18,6 +18,7 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--layers", type=int, default=2)
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--chunk", type=int, default=0)
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 B = args.batch or cfg["B"]
@@ -29,7 +30,8 @@ for layer in range(args.layers):
     cache = PagedKVCache(B, H, G, pages_for(n), dtype=torch.bfloat16)
     batch = make_batch(B, H, G, n, torch.bfloat16, tau=tau_schedule(H, TAUS), seed=1 + layer)
     cache.prefill(batch.K[:, :, : n - 1], batch.V[:, :, : n - 1])
-    dec = TwilightDecoder(cache, cfg["selector"], budget=cfg["budget"], p=cfg["p"], bufs=shared)
+    dec = TwilightDecoder(cache, cfg["selector"], budget=cfg["budget"], p=cfg["p"], bufs=shared,
+                          chunk_tokens=args.chunk or None)
     shared = dec.bufs
     decs.append(dec)
     q, k_new, v_new = batch.q.contiguous(), batch.k_new.contiguous(), batch.v_new.contiguous()
@@ -41,5 +43,6 @@ for d in decs:
 torch.cuda.synchronize()
 ms = stage_breakdown(decs, q, k_new, v_new, pos, out, args.reps)
 print(json.dumps({"lib": os.environ.get("TW_LIB_PATH", "in-tree"), "config": args.config, "B": B,
+                  "chunk": decs[0].params.chunk_tokens,
                   "us": {k: round(v * 1e3, 2) for k, v in ms.items()},
                   "total": round(sum(ms.values()) * 1e3, 2)}))
