@@ -5,87 +5,108 @@
 // returned set is {w >= l}, and with the default epsilon/max_iters the search
 // runs until that set is the MINIMAL TIE-CLOSED top set whose mass reaches
 // p_eff = min(p, sum w) - 1e-9 (break rules :99-104).  We compute that set
-// directly instead of bisecting (~50 passes): a mass-weighted radix select.
+// directly instead of bisecting (~50 passes over the weights): a mass-weighted
+// radix select, split into two grid-wide kernels so that every pass over the
+// logits runs on the whole GPU (not one CTA per head):
 //
-//   pass 1   e_i = exp(z_i - max) (SFU exp2, ~1e-6 relative), quantised to
-//            u64 fixed point (exact, order-independent sums => deterministic);
-//            histogram of (count, mass) over 4096 bins of (max - z) ; the
-//            crossing bin is the first (highest-z) bin where the running mass
-//            reaches p_eff * Z.
-//   pass 2+  the crossing bin's members are compacted to shared memory and
-//            ranked exactly by their fp32 logit key (ties = equal logits =
-//            equal weights); bins too full to rank are split again by key.
-// The selected set is {z >= z_thr}: the same tie-closed set the reference
-// returns, up to weights within ~1e-7 relative of the threshold.
+//   topp_hist   grid (head, 8192-logit chunk).  e_i = exp(z_i - max) is binned
+//               by (max - z) into 4096 bins of 1/120 logit; a bin holds
+//               (count, sum of u32 fixed-point deficits) packed in one u64, so
+//               bin masses are exact, order-independent integer sums (the
+//               result is deterministic).  Chunks merge into a per-head global
+//               histogram with u64 atomics; the head's last chunk CTA finds the
+//               crossing bin (first bin, highest z first, where the running mass
+//               reaches p_eff * Z) and writes the head record.
+//   topp_union  grid (unit, slice of candidate positions).  One read of the G
+//               heads' logits: a position is kept if, for some head, its bin
+//               lies above that head's crossing bin; crossing-bin members go to
+//               a per-unit list.  The unit's last slice CTA ranks each head's
+//               members exactly by fp32 logit key (key buckets, then an exact
+//               rank of <= 64 members; ties = equal logits = equal weights),
+//               adds them to the union bitmap, and compacts the group's final
+//               set (pipeline.py:347) into ascending token ids and attention
+//               work items.
 //
-// K3c: the group's final set is the union over its G heads (pipeline.py:347);
-// it is compacted in ascending token order and cut into attention work items.
+// The selected set is {z >= z_thr}: the reference's tie-closed set, up to
+// weights within ~1e-7 relative of the threshold (SFU exp inside a bin).
+#include <algorithm>
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "block_scan.cuh"
-#ifdef TW_TOPP_TRACE
-#include <cstdio>
-#endif
+
+namespace cg = cooperative_groups;
 
 namespace tw {
 
 #ifdef TW_TOPP_TRACE
-__device__ unsigned long long g_trace[512 * 8];
-__device__ int g_trace_phase[512];
-#define TRACE(tag)                                                                                  \
-  do {                                                                                              \
-    if (threadIdx.x == 0 && blockIdx.x < 512) {                                                     \
-      unsigned long long now;                                                                       \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));                                      \
-      int ph = g_trace_phase[blockIdx.x]++;                                                         \
-      if (ph < 8) g_trace[blockIdx.x * 8 + ph] = now;                                               \
-    }                                                                                               \
+constexpr int kTrCta = 8192;
+__device__ unsigned long long g_tt[3][kTrCta][8];
+#define TT(k, ph)                                                                                    \
+  do {                                                                                               \
+    const int c_ = blockIdx.x + blockIdx.y * gridDim.x;                                              \
+    if (threadIdx.x == 0 && c_ < kTrCta) {                                                           \
+      unsigned long long now_;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));                                      \
+      g_tt[k][c_][ph] = now_;                                                                        \
+    }                                                                                                \
   } while (0)
 #else
-#define TRACE(tag) do {} while (0)
+#define TT(k, ph) do {} while (0)
 #endif
 
-#ifndef TW_TOPP_THREADS
-#define TW_TOPP_THREADS 512
-#endif
-constexpr int kTopThreads = TW_TOPP_THREADS;
-#ifndef TW_TOPP_MINB
-#define TW_TOPP_MINB 2
-#endif
-constexpr int kBins = 4096;
-constexpr int kRankCap = 512;           // members ranked O(k^2) in shared memory
-constexpr float kBinPerLogit = 120.0f;  // bins cover (max - z) in [0, 34.1)
-constexpr int kNW = kTopThreads / 32;
-constexpr int kPer = kBins / kTopThreads;
-static_assert(kPer <= 8, "find_crossing's step table covers 8 bins per thread");
-// exp(-i/120), i = 0..7
-__device__ constexpr double kStepExp[8] = {1.0, 0.991701292638876, 0.9834714538216175, 0.9753099120283326,
-                                           0.9672161004820059, 0.9591894571091382, 0.951229424500714,
-                                           0.9433354498734922};
+constexpr int kBins = TW_TOPP_BINS;      // 4096
+constexpr float kBinPerLogit = 120.0f;   // bins cover (max - z) in [0, 34.1); the last bin takes the rest
+constexpr int kTT = 256;                 // threads of both kernels
+constexpr int kTW = kTT / 32;
+constexpr int kPerT = kBins / kTT;       // 16 bins per thread in the scans
+constexpr int kClusterLogits = 16384;    // candidate positions per histogram CTA (cluster size)
+constexpr int kUnionLogits = 16384;      // logits (positions x G) per union CTA
+constexpr int kMemberCap = TW_TOPP_MEMBER_CAP;
+constexpr uint64_t kCntOne = 1ull << 43; // packed bin: count << 43 | deficit sum
+constexpr uint64_t kUsMask = kCntOne - 1;
+constexpr float kUscale = 4194304.0f;    // deficits in units of 2^-22
+constexpr double kInvUscale = 1.0 / 4194304.0;
+// exp(-i/120), i = 0..15
+__constant__ double kStepExp[16] = {
+    1.0, 0.991701292638876, 0.9834714538216175, 0.9753099120283326, 0.9672161004820059, 0.9591894571091382,
+    0.951229424500714, 0.9433354498734922, 0.9355069850316178, 0.9277434863285529, 0.9200444146293233,
+    0.9124092352730778, 0.9048374180359595, 0.8973284370942841, 0.8898817709880238, 0.8824969025845955};
+
+// Per-head record written by topp_hist, read by topp_union.
+struct TopHead {
+  double above_mass;  // mass of the bins above the crossing bin
+  double target;      // p_eff * Z
+  double Z;           // total mass (in units of exp(z - max))
+  double wb;          // weight of the crossing bin's top, exp(t_cb - max)
+  int32_t cb;         // crossing bin; -1: keep every candidate; -2: keep nothing
+  uint32_t above_cnt, members, b0;
+  float M;            // max logit
+  float zhi, zlo;     // crossing bin = (zlo, zhi] in logit space: kept outright iff z > zhi
+  uint32_t pad;
+};
+static_assert(sizeof(TopHead) == TW_TOPP_HEAD_BYTES, "head record size");
 
 // Masses.  Bin b of (max - z) has top t_b = M - b/120 (float) and weight
 // w_b = exp(t_b - M) (fp64).  A member has e_i = exp(z_i - M) = w_b r_i with
-// r_i = exp(z_i - t_b) in (0.9917, 1]; it is summed as the u32 fixed-point
-// deficit u_i = rint((1 - r_i) 2^kq) (< 2^kq / 120), so
-//     bin mass = w_b (count - sum u / 2^kq).
-// Counts and deficits are plain u32 shared-memory adds (no 64-bit carries),
-// exact and order-independent => deterministic.  r_i comes from the SFU over
-// a 1/120-logit range (~2e-7 relative); w_b is fp64.  The deepest bin (34+
-// logits below the max, weights < 2e-15) takes whatever lands there.
+// r_i = exp(z_i - t_b) in (0.9917, 1]; it is summed as the fixed-point deficit
+// u_i = rint((1 - r_i) 2^22), so bin mass = w_b (count - sum u / 2^22).  r_i
+// comes from the SFU over a 1/120-logit range (~2e-7 relative); w_b is fp64.
+// The deepest bin (34+ logits below the max, weights < 2e-15) takes whatever
+// lands there.
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-
-// bin of z: floor((M - z) * 120), clamped to the last bin
 __device__ __forceinline__ int dbin(float z, float M120) {
   return min(__float2int_rz(fmaf(-z, kBinPerLogit, M120)), kBins - 1);
 }
-
-// Largest float z with dbin(z) >= b (dbin is non-increasing in z), so bin b is
-// the float interval (bin_ceiling(b + 1), bin_ceiling(b)].
-__device__ __forceinline__ float bin_ceiling(int b, float M, float M120) {
+__device__ __forceinline__ float bin_top(float M, int b) { return fmaf(-(float)b, 1.0f / kBinPerLogit, M); }
+// Largest float z with dbin(z) >= b (dbin is non-increasing in z), so bin b
+// is the float interval (bin_ceiling(b + 1), bin_ceiling(b)].
+__device__ float bin_ceiling(int b, float M, float M120) {
   if (b <= 0) return INFINITY;
   if (b >= kBins) return -INFINITY;
   float e = M - (float)b / kBinPerLogit;
@@ -97,408 +118,673 @@ __device__ __forceinline__ float bin_ceiling(int b, float M, float M120) {
   }
   return e;
 }
-
-__device__ __forceinline__ float bin_top(float M, int b) { return fmaf(-(float)b, 1.0f / kBinPerLogit, M); }
-
-__device__ __forceinline__ uint32_t deficit(float z, float M, int b, float uscale) {
+__device__ __forceinline__ uint32_t deficit(float z, float M, int b) {
   const float r = ex2_approx((z - bin_top(M, b)) * 1.4426950408889634f);
-  return (uint32_t)__float2int_rn(fmaxf(fmaf(-r, uscale, uscale), 0.0f));
+  return (uint32_t)__float2int_rn(fmaxf(fmaf(-r, kUscale, kUscale), 0.0f));
 }
-
-__device__ __forceinline__ double class_mass(double w, uint64_t cnt, uint64_t usum, double inv_uscale) {
-  return w * ((double)cnt - (double)usum * inv_uscale);
+__device__ __forceinline__ double class_mass(double w, uint64_t cnt, uint64_t usum) {
+  return w * ((double)cnt - (double)usum * kInvUscale);
 }
+__device__ __forceinline__ float4 ninf4() { return make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY); }
+__device__ __forceinline__ float comp(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
 
-// CTA-wide inclusive scan with a compile-time warp count.
+// CTA-wide (kTT threads) inclusive scan.
 template <typename T>
-__device__ __forceinline__ T cta_incl_scan(T v, T* tmp, T& total) {
+__device__ __forceinline__ T cta_scan(T v, T* tmp, T& total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   T x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    T y = __shfl_up_sync(0xffffffffu, x, o);
+    const T y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
   if (lane == 31) tmp[wid] = x;
   __syncthreads();
-  if (wid == 0) {
-    T s = lane < kNW ? tmp[lane] : T(0);
+  T pre = T(0), tot = T(0);
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      T y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
-    }
-    if (lane < kNW) tmp[lane] = s;
+  for (int i = 0; i < kTW; ++i) {
+    const T s = tmp[i];
+    pre += i < wid ? s : T(0);
+    tot += s;
   }
   __syncthreads();
-  if (wid > 0) x += tmp[wid - 1];
-  total = tmp[kNW - 1];
-  __syncthreads();
-  return x;
+  total = tot;
+  return x + pre;
+}
+template <typename T>
+__device__ __forceinline__ T cta_sum(T v, T* tmp) {
+  T total;
+  cta_scan<T>(v, tmp, total);
+  return total;
 }
 
-struct TopSmem {
-  uint32_t cnt[kBins];
-  uint32_t usum[kBins];
-  uint32_t mkey[kRankCap];
-  uint32_t mu[kRankCap];
-  double dtmp[32];
-  uint32_t utmp[32];
-  int nmem;
-  uint32_t kmin, kmax;
+struct ScanSmem {
+  double dtmp[kTW];
+  uint32_t utmp[kTW];
+  uint64_t ltmp[kTW];
   int bin;
-  double above_mass;
+  double above;
   uint32_t above_cnt;
-  uint32_t thr;
-  uint32_t selc;
-  unsigned long long selu;
 };
 
-// First bin in priority order whose running mass (from base_mass) reaches
-// the target.  Level 0 (wconst <= 0): bins of (max - z) weighted w_b,
-// priority = ascending b, target = p_eff * (total mass), returned as Z.
-// Deeper levels: key sub-bins of one parent bin, all weighted wconst,
-// priority = descending index (highest key first).  Also returns the count
-// of everything scanned in `count_total`.
-__device__ __forceinline__ double find_crossing(TopSmem& S, double target, double base_mass, float M, double wconst,
-                                                double inv_uscale, double p_eff, uint32_t& count_total) {
-  const bool level0 = !(wconst > 0.0);
-  double m[kPer];
-  uint32_t c[kPer];
-  double w0 = wconst;
-  float t0 = 0.f;
-  if (level0) {  // w_b for this thread's kPer consecutive bins: one exp, then exact small-step corrections
-    t0 = bin_top(M, threadIdx.x * kPer);
-    w0 = exp((double)t0 - (double)M);
-  }
+// First entry, in priority order (thread-major, then i), whose running mass
+// from `base` reaches `target`: -> S.bin (= rank, or -1), S.above, S.above_cnt.
+// `entry(i, m, c)` gives the mass and count of the thread's i-th entry (it is
+// evaluated twice instead of holding 16 doubles live).  Returns the total
+// mass; `ctot` receives the total count.
+template <class Entry>
+__device__ __forceinline__ double scan_crossing(Entry&& entry, double base, double target, bool target_is_fraction,
+                                                ScanSmem& S, uint32_t& ctot, double& target_out) {
   double local = 0.0;
-  uint32_t lcnt = 0;
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const int rank = threadIdx.x * kPer + i;
-    const int bb = level0 ? rank : (kBins - 1 - rank);
-    c[i] = S.cnt[bb];
-    double w = wconst;
-    if (level0) {
-      // exp(t_b - M) = w0 * exp(t_b - t0);  t_b - t0 = -i/120 + d (d ~ float rounding, tiny)
-      const double d = ((double)bin_top(M, bb) - (double)t0) + (double)i / (double)kBinPerLogit;
-      w = w0 * kStepExp[i] * (1.0 + d * (1.0 + 0.5 * d));
-    }
-    m[i] = c[i] ? class_mass(w, c[i], S.usum[bb], inv_uscale) : 0.0;
-    local += m[i];
-    lcnt += c[i];
+  uint32_t lc = 0;
+#pragma unroll 4
+  for (int i = 0; i < kPerT; ++i) {
+    double m;
+    uint32_t c;
+    entry(i, m, c);
+    local += m;
+    lc += c;
   }
   double total;
-  const double incl = cta_incl_scan<double>(local, S.dtmp, total);
-  uint32_t ctot;
-  const uint32_t cincl = cta_incl_scan<uint32_t>(lcnt, S.utmp, ctot);
-  count_total = ctot;
-  if (level0) target = p_eff * total;
-  const double excl = incl - local;
+  const double incl = cta_scan<double>(local, S.dtmp, total);
+  const uint32_t cincl = cta_scan<uint32_t>(lc, S.utmp, ctot);
+  if (target_is_fraction) target *= total;
+  target_out = target;
   if (threadIdx.x == 0) S.bin = -1;
   __syncthreads();
-  if (base_mass + excl < target && target <= base_mass + incl) {
-    double run = base_mass + excl;
-    uint32_t crun = cincl - lcnt;
-    bool found = false;
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      if (!found && c[i] && run + m[i] >= target) {
-        found = true;
-        S.bin = level0 ? threadIdx.x * kPer + i : kBins - 1 - (threadIdx.x * kPer + i);
-        S.above_mass = run;
+  const double excl = incl - local;
+  if (base + excl < target && target <= base + incl) {
+    double run = base + excl;
+    uint32_t crun = cincl - lc;
+#pragma unroll 1
+    for (int i = 0; i < kPerT; ++i) {
+      double m;
+      uint32_t c;
+      entry(i, m, c);
+      if (c && run + m >= target) {
+        S.bin = threadIdx.x * kPerT + i;
+        S.above = run;
         S.above_cnt = crun;
+        break;
       }
-      run += m[i];
-      crun += c[i];
+      run += m;
+      crun += c;
     }
   }
   __syncthreads();
   return total;
 }
 
-// Vectorised walk over a head's logits: kUnroll float4 in flight per thread.
-#ifndef TW_TOPP_UNROLL
-#define TW_TOPP_UNROLL 4
-#endif
-constexpr int kUnroll = TW_TOPP_UNROLL;
-template <typename F>
-__device__ __forceinline__ void for_each_logit(const float* __restrict__ z, int npos, F&& f) {
-  const float4* z4 = reinterpret_cast<const float4*>(z);
-  const int n4 = npos >> 2;
-  for (int base = threadIdx.x; base < n4; base += kTopThreads * kUnroll) {
-    float4 v[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int i = base + u * kTopThreads;
-      v[u] = i < n4 ? __ldcg(z4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+// ---------------------------------------------------------------- K3b-1: histogram + crossing bin
+
+// grid (cluster size cs, Hq), cluster (cs, 1, 1): CTA `rank` of a head's
+// cluster bins positions [rank * chunk, (rank + 1) * chunk); the per-CTA bins
+// are merged through distributed shared memory (each rank sums a 1/cs slice of
+// the bins over the cluster into rank 0), and rank 0 finds the crossing bin.
+__global__ void __launch_bounds__(kTT, 4) topp_hist_kernel(tw_paged_kv kv, tw_decode_params prm, tw_decode_buffers buf) {
+  // per-CTA bins as two u32 arrays (native shared atomics; a u64 shared add
+  // is a CAS loop on sm_100a).  A regular bin's deficits are < 2^22/120 each;
+  // the deepest bin's (up to 2^22 each) go to a u64.
+  __shared__ uint32_t Hc[kBins], Hu[kBins];
+  __shared__ unsigned long long s_deep;
+  __shared__ ScanSmem S;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cs = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int qh = blockIdx.y, tid = threadIdx.x;
+  const int unit = qh / kv.group_size;
+  const int npos = buf.cand_count[unit] * kPage;
+  TopHead* rec = reinterpret_cast<TopHead*>(buf.topp_heads) + qh;
+  const float M = key2f(buf.head_max[qh]);  // NaN when the head has no valid logit
+  const double p_eff = fmin(prm.p, 1.0) - 1e-9;
+  if (p_eff <= 0.0 || npos == 0 || !(M > -INFINITY)) {  // uniform over the cluster: nobody syncs
+    if (rank == 0 && tid == 0) {
+      TopHead r{};
+      r.cb = -2;
+      r.M = M;
+      r.zhi = r.zlo = INFINITY;
+      *rec = r;
     }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      f(v[u].x);
-      f(v[u].y);
-      f(v[u].z);
-      f(v[u].w);
-    }
+    return;
   }
+  TT(0, 0);
+  const float M120 = M * kBinPerLogit;
+  for (int i = tid; i < kBins; i += kTT) Hc[i] = Hu[i] = 0;
+  if (tid == 0) s_deep = 0;
+  __syncthreads();
+  TT(0, 1);
+  {
+    const size_t T = (size_t)kv.max_pages * kPage;
+    const int chunk = ((npos + cs - 1) / cs + 1023) & ~1023;  // even split of the head's positions
+    const int lo = rank * chunk, hi = min(npos, lo + chunk);
+    const float4* z4 = reinterpret_cast<const float4*>(buf.logits + (size_t)qh * T);
+    unsigned long long deep = 0;
+    for (int p0 = lo; p0 < hi; p0 += 16 * kTT) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = p0 + 4 * (tid + u * kTT);
+        v[u] = p < hi ? __ldcg(z4 + (p >> 2)) : ninf4();
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float z = comp(v[u], e);
+          if (z > -INFINITY) {
+            const int b = dbin(z, M120);
+            const uint32_t d = deficit(z, M, b);
+            atomicAdd(&Hc[b], 1u);
+            if (b < kBins - 1) atomicAdd(&Hu[b], d);
+            else deep += d;
+          }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) deep += __shfl_xor_sync(0xffffffffu, deep, o);
+    if ((tid & 31) == 0 && deep) atomicAdd(&s_deep, deep);
+  }
+  TT(0, 2);
+  if (cs > 1) {
+    cluster.sync();
+    TT(0, 3);
+    // rank r sums bins [r * 4096 / cs, (r + 1) * 4096 / cs) over the cluster into rank 0
+    const int per = kBins / cs;
+    const uint32_t* rc[8];
+    const uint32_t* ru[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      rc[r] = cluster.map_shared_rank(Hc, r < cs ? r : 0);
+      ru[r] = cluster.map_shared_rank(Hu, r < cs ? r : 0);
+    }
+    uint32_t* c0 = cluster.map_shared_rank(Hc, 0);
+    uint32_t* u0 = cluster.map_shared_rank(Hu, 0);
+    for (int i = rank * per + tid; i < (rank + 1) * per; i += kTT) {
+      uint32_t c[8], u[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        c[r] = r < cs ? rc[r][i] : 0u;
+        u[r] = r < cs ? ru[r][i] : 0u;
+      }
+      uint32_t cc = 0, uu = 0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) { cc += c[r]; uu += u[r]; }
+      c0[i] = cc;
+      u0[i] = uu;
+    }
+    TT(0, 7);
+    if (rank == cs - 1 && tid == 0) {
+      unsigned long long d = 0;
+      for (int r = 0; r < cs; ++r) d += *cluster.map_shared_rank(&s_deep, r);
+      *cluster.map_shared_rank(&s_deep, 0) = d;
+    }
+    cluster.sync();
+    TT(0, 4);
+    if (rank != 0) return;
+  }
+  auto packed = [&](int i) -> uint64_t {
+    return ((uint64_t)Hc[i] << 43) | (i == kBins - 1 ? (uint64_t)s_deep : (uint64_t)Hu[i]);
+  };
+  // masses of this thread's 16 consecutive bins: one exp, then exact small steps
+  const int bfirst = tid * kPerT;
+  const float t0 = bin_top(M, bfirst);
+  const double w0 = exp((double)t0 - (double)M);
+  auto entry = [&](int i, double& m, uint32_t& c) {
+    const int bb = bfirst + i;
+    c = Hc[bb];
+    // exp(t_b - M) = w0 * exp(t_b - t0);  t_b - t0 = -i/120 + d (d ~ float rounding, tiny)
+    const double d = ((double)bin_top(M, bb) - (double)t0) + (double)i * (1.0 / 120.0);
+    const double w = w0 * kStepExp[i] * (1.0 + d * (1.0 + 0.5 * d));
+    m = c ? class_mass(w, c, packed(bb) & kUsMask) : 0.0;
+  };
+  uint32_t b0;
+  double target;
+  const double Z = scan_crossing(entry, 0.0, p_eff, true, S, b0, target);
+  TT(0, 6);
+  if (tid == 0) {
+    TopHead r{};
+    r.cb = S.bin;  // -1: rounding left the target above the total -> keep everything
+    r.above_mass = S.bin >= 0 ? S.above : 0.0;
+    r.above_cnt = S.bin >= 0 ? S.above_cnt : 0u;
+    r.members = S.bin >= 0 ? Hc[S.bin] : 0u;
+    r.b0 = b0;
+    r.Z = Z;
+    r.target = target;
+    r.wb = S.bin >= 0 ? exp((double)bin_top(M, S.bin) - (double)M) : 0.0;
+    r.M = M;
+    r.zhi = S.bin >= 0 ? bin_ceiling(S.bin, M, M120) : -INFINITY;
+    r.zlo = S.bin >= 0 ? bin_ceiling(S.bin + 1, M, M120) : -INFINITY;
+    *rec = r;
+  }
+  TT(0, 5);
 }
 
-// One CTA per query head; the last head of a unit to finish also forms the
-// group's final set (K3c) and reserves its attention work items.
-__global__ void __launch_bounds__(kTopThreads, TW_TOPP_MINB) topp_head_kernel(tw_paged_kv kv, tw_decode_params prm,
-                                                                               tw_decode_buffers buf) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TopSmem& S = *reinterpret_cast<TopSmem*>(smem_raw);
-  __shared__ int s_last;
-  const int qh = blockIdx.x;
-  const int G = kv.group_size;
-  const int unit = qh / G;
+// ---------------------------------------------------------------- K3b-2: union scan
+
+// One read of the G heads' logits over a slice of candidate positions: a
+// position is in the union bitmap if some head keeps it outright (bin above
+// the head's crossing bin); crossing-bin members are appended to the unit's
+// member list as (key << 32 | head << 24 | position).
+template <int G>
+__global__ void __launch_bounds__(kTT, 3) topp_union_kernel(tw_paged_kv kv, tw_decode_buffers buf) {
+  constexpr int kSlice = kUnionLogits / G;  // candidate positions per CTA
+  __shared__ float s_hi[G], s_lo[G];
+  const int unit = blockIdx.y, slice = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const int npos = buf.cand_count[unit] * kPage;
-  const size_t T = (size_t)kv.max_pages * kPage;
-  const float* z = buf.logits + (size_t)qh * T;
-  const float M = key2f(buf.head_max[qh]);
-  const float M120 = M * kBinPerLogit;
-  const double p_eff = fmin(prm.p, 1.0) - 1e-9;
-  float* stats = buf.head_stats + (size_t)qh * 4;
-  uint32_t thr = 0xFFFFFFFFu;  // selects nothing
-  uint32_t b0 = 0;
-  double Z = 0.0;
-  uint32_t sel_cnt = 0;        // |{z >= thr}|   (from the histograms, no extra pass)
-  double sel_mass = 0.0;       // its mass
-  // deficit scale: a bin's u32 sum holds up to 2^32 / (2^kq / 120) members
-  const float uscale = npos > 120000 ? 1048576.0f : 4194304.0f;
-  const double inv_uscale = 1.0 / (double)uscale;
-  const bool empty = p_eff <= 0.0 || npos == 0 || !(M > -INFINITY);
-  TRACE("start");
-  if (!empty) {
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      S.cnt[threadIdx.x + i * kTopThreads] = 0;
-      S.usum[threadIdx.x + i * kTopThreads] = 0;
+  const int base = slice * kSlice;
+  if (base >= npos) return;
+  TT(1, 0);
+  if (tid == 0) {
+    // heads whose crossing-bin members fit the unit's list (greedy, in head order); the
+    // others get an empty member range and are resolved by re-reading their logits
+    const TopHead* R = reinterpret_cast<const TopHead*>(buf.topp_heads) + (size_t)unit * G;
+    uint32_t acc = 0;
+    for (int g = 0; g < G; ++g) {
+      const bool in = R[g].cb >= 0 && acc + R[g].members <= (uint32_t)kMemberCap;
+      if (in) acc += R[g].members;
+      s_hi[g] = R[g].zhi;
+      s_lo[g] = in ? R[g].zlo : R[g].zhi;
     }
+  }
+  __syncthreads();
+  float zhi[G], zlo[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) { zhi[g] = s_hi[g]; zlo[g] = s_lo[g]; }
+  const size_t T = (size_t)kv.max_pages * kPage;
+  const float* zu = buf.logits + (size_t)unit * G * T;
+  uint32_t* ubits = buf.sel_bits + (size_t)unit * (T / 32);
+  uint64_t* mem = buf.topp_members + (size_t)unit * kMemberCap;
+  uint32_t* mcount = reinterpret_cast<uint32_t*>(buf.topp_ctr) + unit;
+  const int len = min(kSlice, npos - base);
+  constexpr int kIters = kSlice / (4 * kTT);
+  float4 v[kIters][G];
+#pragma unroll
+  for (int it = 0; it < kIters; ++it) {
+    const int p0 = 4 * tid + it * 4 * kTT;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      v[it][g] = p0 < len ? __ldcg(reinterpret_cast<const float4*>(zu + g * T + base + p0)) : ninf4();
+  }
+  uint32_t nmem = 0;
+#pragma unroll
+  for (int it = 0; it < kIters; ++it) {
+    const int p0 = 4 * tid + it * 4 * kTT;
+    const int p = base + p0;
+    uint32_t nib = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float z = comp(v[it][g], e);
+        nib |= (z > zhi[g] ? 1u : 0u) << e;
+        nmem += (z > zlo[g]) & (z <= zhi[g]);
+      }
+    }
+    uint32_t w = nib << (4 * (lane & 7));
+    w |= __shfl_xor_sync(0xffffffffu, w, 1);
+    w |= __shfl_xor_sync(0xffffffffu, w, 2);
+    w |= __shfl_xor_sync(0xffffffffu, w, 4);
+    if ((lane & 7) == 0 && p0 < len) ubits[p >> 5] = w;
+  }
+  TT(1, 1);
+  // crossing-bin members: one list reservation per CTA
+  __shared__ uint32_t s_tmp[kTT / 32];
+  __shared__ uint32_t s_base;
+  uint32_t total;
+  const uint32_t incl = cta_scan<uint32_t>(nmem, s_tmp, total);
+  if (total) {
+    if (tid == 0) s_base = atomicAdd(mcount, total);
     __syncthreads();
-    for_each_logit(z, npos, [&](float zi) {
-      if (zi > -INFINITY) {
-        const int bb = dbin(zi, M120);
-        atomicAdd(&S.cnt[bb], 1u);
-        atomicAdd(&S.usum[bb], deficit(zi, M, bb, uscale));
+    TT(1, 2);
+    uint32_t slot = s_base + incl - nmem;
+    if (nmem) {
+#pragma unroll
+      for (int it = 0; it < kIters; ++it) {
+        const int p = base + 4 * tid + it * 4 * kTT;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float z = comp(v[it][g], e);
+            if (z > zlo[g] && z <= zhi[g]) {
+              if (slot < (uint32_t)kMemberCap)
+                mem[slot] = ((uint64_t)f2key(z) << 32) | ((uint64_t)g << 24) | (uint64_t)(p + e);
+              ++slot;
+            }
+          }
+        }
+      }
+    }
+  }
+  TT(1, 3);
+}
+
+// ---------------------------------------------------------------- K3b-3 / K3c: exact thresholds + group union
+
+constexpr int kResThreads = 512;
+constexpr int kResBuckets = 1024;  // key buckets per level
+constexpr int kRankCap = 64;       // members ranked exactly (O(k^2))
+
+template <typename T>
+__device__ __forceinline__ T grp_scan(const Group& g, T v, T* tmp, T& total) {
+  const int lane = g.tid & 31, wid = g.warp(), nw = g.nwarps();
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[wid] = x;
+  g.sync();
+  T pre = T(0), tot = T(0);
+  for (int i = 0; i < nw; ++i) {
+    const T s = tmp[i];
+    pre += i < wid ? s : T(0);
+    tot += s;
+  }
+  g.sync();
+  total = tot;
+  return x + pre;
+}
+
+struct ResGroupSmem {
+  uint32_t bc[kResBuckets];
+  unsigned long long bu[kResBuckets];
+  uint32_t rk[kRankCap], ru[kRankCap];
+  double dtmp[16];
+  uint32_t utmp[16];
+  unsigned long long ltmp[16];
+  uint32_t kmin, kmax, live, thr;
+  int nr, bin;
+  double above;
+};
+
+// members of one head's crossing bin: a segment of the shared member list ...
+struct SmemSrc {
+  const uint32_t* keys;
+  const uint32_t* pos;
+  int m;
+  float M;
+  int cb;
+  template <class F>
+  __device__ __forceinline__ void each(const Group& g, F&& f) const {
+    for (int i = g.tid; i < m; i += g.nthreads) {
+      const uint32_t k = keys[i];
+      f(k, deficit(key2f(k), M, cb), pos[i]);
+    }
+  }
+};
+// ... or, when the list overflowed, found again by re-reading the head's logits
+struct LogitSrc {
+  const float* z;
+  int npos;
+  float M;
+  int cb;
+  template <class F>
+  __device__ __forceinline__ void each(const Group& g, F&& f) const {
+    const float4* z4 = reinterpret_cast<const float4*>(z);
+    const float M120 = M * kBinPerLogit;
+    for (int i = g.tid; i < (npos >> 2); i += g.nthreads) {
+      const float4 v = __ldcg(z4 + i);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float x = comp(v, e);
+        if (x > -INFINITY && dbin(x, M120) == cb) f(f2key(x), deficit(x, M, cb), (uint32_t)(4 * i + e));
+      }
+    }
+  }
+};
+
+// Threshold key inside the crossing bin: the key of the class at which the
+// running mass (highest key first, from `base`) reaches `target`.  Members
+// share the bin weight wb, so a class's mass is wb (count - sum u / 2^22).
+template <class Src>
+__device__ uint32_t resolve_threshold(const Group& g, const Src& src, double base, double target, double wb,
+                                      ResGroupSmem& S) {
+  const int lane = g.tid & 31;
+  uint32_t klo = 0, khi = 0xFFFFFFFFu;
+  for (int level = 0; level < 6; ++level) {
+    if (g.tid == 0) { S.kmin = 0xFFFFFFFFu; S.kmax = 0; S.live = 0; S.nr = 0; S.bin = -1; }
+    g.sync();
+    uint32_t lmin = 0xFFFFFFFFu, lmax = 0, lc = 0;
+    src.each(g, [&](uint32_t k, uint32_t, uint32_t) {
+      if (k >= klo && k <= khi) { lmin = min(lmin, k); lmax = max(lmax, k); ++lc; }
+    });
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+      lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+      lc += __shfl_xor_sync(0xffffffffu, lc, o);
+    }
+    if (lane == 0 && lc) { atomicMin(&S.kmin, lmin); atomicMax(&S.kmax, lmax); atomicAdd(&S.live, lc); }
+    g.sync();
+    const uint32_t kmin = S.kmin, kmax = S.kmax, live = S.live;
+    if (live == 0) return klo;
+    if (kmin == kmax) return kmin;  // one tie class fills the range: it is the threshold
+    if (live <= kRankCap) {
+      src.each(g, [&](uint32_t k, uint32_t u, uint32_t) {
+        if (k >= klo && k <= khi) {
+          const int s = atomicAdd(&S.nr, 1);
+          S.rk[s] = k;
+          S.ru[s] = u;
+        }
+      });
+      if (g.tid == 0) S.thr = kmin;  // rounding fallback: keep the whole range
+      g.sync();
+      for (int a = g.tid; a < (int)live; a += g.nthreads) {
+        const uint32_t ka = S.rk[a];
+        uint32_t cgt = 0, ceq = 0;
+        uint64_t ugt = 0, ueq = 0;
+        for (int j = 0; j < (int)live; ++j) {
+          const uint32_t kj = S.rk[j], uj = S.ru[j];
+          cgt += kj > ka;
+          ugt += kj > ka ? uj : 0u;
+          ceq += kj == ka;
+          ueq += kj == ka ? uj : 0u;
+        }
+        const double lo = base + class_mass(wb, cgt, ugt);
+        const double hi = lo + class_mass(wb, ceq, ueq);
+        if (lo < target && target <= hi) S.thr = ka;  // every writer of this class writes the same key
+      }
+      g.sync();
+      return S.thr;
+    }
+    // split the live range into key buckets, highest key first
+    const int sh = max(0, (32 - __clz(kmax - kmin)) - 10);
+    for (int i = g.tid; i < kResBuckets; i += g.nthreads) { S.bc[i] = 0; S.bu[i] = 0; }
+    g.sync();
+    src.each(g, [&](uint32_t k, uint32_t u, uint32_t) {
+      if (k >= klo && k <= khi) {
+        const int bk = (int)((k - kmin) >> sh);
+        atomicAdd(&S.bc[bk], 1u);
+        atomicAdd(&S.bu[bk], (unsigned long long)u);
       }
     });
-    __syncthreads();
-    TRACE("pass1");
-    Z = find_crossing(S, 0.0, 0.0, M, 0.0, inv_uscale, p_eff, b0);
-    const double target = p_eff * Z;
-    TRACE("crossing");
-    int bin = S.bin;
-    double above_mass = S.above_mass;
-    uint32_t above_cnt = S.above_cnt;
-    uint32_t klo = 0, khi = 0xFFFFFFFFu;
-    bool resolved = false;
-    if (bin < 0) {  // rounding: the whole set is needed
-      thr = 0;
-      sel_cnt = b0;
-      sel_mass = Z;
-      resolved = true;
+    g.sync();
+    const int per = kResBuckets / g.nthreads;  // buckets per thread, highest key first
+    double local = 0.0;
+    for (int i = 0; i < per; ++i) {
+      const int bk = kResBuckets - 1 - (g.tid * per + i);
+      local += S.bc[bk] ? class_mass(wb, S.bc[bk], S.bu[bk]) : 0.0;
     }
-    const int pbin = bin;  // parent bin of every deeper level
-    __shared__ float s_zr[2];
-    if (!resolved && threadIdx.x == 0) {
-      s_zr[0] = bin_ceiling(pbin + 1, M, M120);  // members: zlo < z <= zhi
-      s_zr[1] = bin_ceiling(pbin, M, M120);
-    }
-    __syncthreads();
-    const float zlo = s_zr[0], zhi = s_zr[1];
-    const double wb = resolved ? 0.0 : exp((double)bin_top(M, pbin) - (double)M);
-    int members = resolved ? 0 : (int)S.cnt[bin];
-    double range_mass = resolved ? 0.0 : class_mass(wb, S.cnt[bin], S.usum[bin], inv_uscale);
-    while (!resolved) {
-      __syncthreads();
-      if (members <= kRankCap) {
-        // compact the members, then rank them exactly
-        if (threadIdx.x == 0) { S.nmem = 0; S.selc = 0; S.selu = 0; }
-        __syncthreads();
-        for_each_logit(z, npos, [&](float zi) {
-          if (zi > zlo && zi <= zhi) {
-            const uint32_t k = f2key(zi);
-            if (k >= klo && k <= khi) {
-              const int slot = atomicAdd(&S.nmem, 1);
-              if (slot < kRankCap) {
-                S.mkey[slot] = k;
-                S.mu[slot] = deficit(zi, M, pbin, uscale);
-              }
-            }
-          }
-        });
-        __syncthreads();
-        TRACE("members");
-        const int nm = min(S.nmem, kRankCap);
-        if (threadIdx.x == 0) S.thr = klo;  // fallback (rounding): keep the whole range
-        __syncthreads();
-        for (int a = threadIdx.x; a < nm; a += kTopThreads) {
-          const uint32_t ka = S.mkey[a];
-          uint32_t cgt = 0, ceq = 0;
-          uint64_t ugt = 0, ueq = 0;
-          for (int j = 0; j < nm; ++j) {
-            const uint32_t kj = S.mkey[j];
-            const uint32_t uj = S.mu[j];
-            cgt += kj > ka;
-            ugt += kj > ka ? uj : 0u;
-            ceq += kj == ka;
-            ueq += kj == ka ? uj : 0u;
-          }
-          const double lo = above_mass + class_mass(wb, cgt, ugt, inv_uscale);
-          const double hi = lo + class_mass(wb, ceq, ueq, inv_uscale);
-          if (lo < target && target <= hi) S.thr = ka;  // every writer of this class writes the same key
-        }
-        __syncthreads();
-        thr = S.thr;
-        for (int a = threadIdx.x; a < nm; a += kTopThreads)
-          if (S.mkey[a] >= thr) {
-            atomicAdd(&S.selc, 1u);
-            atomicAdd(&S.selu, (unsigned long long)S.mu[a]);
-          }
-        __syncthreads();
-        TRACE("ranked");
-        sel_cnt = above_cnt + S.selc;
-        sel_mass = above_mass + class_mass(wb, S.selc, S.selu, inv_uscale);
-        resolved = true;
-      } else {
-        // split the range by key: min/max key of the members, 4096 key sub-bins
-        if (threadIdx.x == 0) { S.kmin = 0xFFFFFFFFu; S.kmax = 0; }
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-          S.cnt[threadIdx.x + i * kTopThreads] = 0;
-          S.usum[threadIdx.x + i * kTopThreads] = 0;
-        }
-        __syncthreads();
-        for_each_logit(z, npos, [&](float zi) {
-          if (zi > zlo && zi <= zhi) {
-            const uint32_t k = f2key(zi);
-            if (k >= klo && k <= khi) {
-              atomicMin(&S.kmin, k);
-              atomicMax(&S.kmax, k);
-            }
-          }
-        });
-        __syncthreads();
-        const uint32_t kmin = S.kmin, kmax = S.kmax;
-        if (kmin == kmax) {  // one tie class fills the range: it is the threshold
-          thr = kmin;
-          sel_cnt = above_cnt + members;
-          sel_mass = above_mass + range_mass;
+    double total;
+    const double incl = grp_scan<double>(g, local, S.dtmp, total);
+    const double excl = incl - local;
+    if (base + excl < target && target <= base + incl) {
+      double run = base + excl;
+      for (int i = 0; i < per; ++i) {
+        const int bk = kResBuckets - 1 - (g.tid * per + i);
+        const double mb = S.bc[bk] ? class_mass(wb, S.bc[bk], S.bu[bk]) : 0.0;
+        if (S.bc[bk] && run + mb >= target) {
+          S.bin = bk;
+          S.above = run;
           break;
         }
-        const int sh = max(0, (32 - __clz(kmax - kmin)) - 12);
-        for_each_logit(z, npos, [&](float zi) {
-          if (zi > zlo && zi <= zhi) {
-            const uint32_t k = f2key(zi);
-            if (k >= klo && k <= khi) {
-              const int sb = (int)((k - kmin) >> sh);
-              atomicAdd(&S.cnt[sb], 1u);
-              atomicAdd(&S.usum[sb], deficit(zi, M, pbin, uscale));
-            }
-          }
-        });
-        __syncthreads();
-        uint32_t dummy;
-        find_crossing(S, target, above_mass, M, wb, inv_uscale, p_eff, dummy);  // highest key first
-        if (S.bin < 0) {
-          thr = kmin;
-          sel_cnt = above_cnt + members;
-          sel_mass = above_mass + range_mass;
-          break;
-        }
-        const int sb = S.bin;
-        above_mass = S.above_mass;
-        above_cnt += S.above_cnt;
-        members = (int)S.cnt[sb];
-        range_mass = class_mass(wb, S.cnt[sb], S.usum[sb], inv_uscale);
-        klo = kmin + ((uint32_t)sb << sh);
-        khi = min(kmax, klo + ((1u << sh) - 1u));
+        run += mb;
       }
     }
-    __syncthreads();
+    g.sync();
+    if (S.bin < 0) return kmin;  // rounding: keep the whole range
+    base = S.above;
+    klo = kmin + ((uint32_t)S.bin << sh);
+    khi = kmax - klo > (1u << sh) - 1u ? klo + ((1u << sh) - 1u) : kmax;
+    g.sync();
   }
-  TRACE("resolved");
-  // selection bitmap of the head's pruned set {z >= z_thr} (float compares; -inf never selected)
-  uint32_t* bits = buf.sel_bits + (size_t)qh * (T / 32);
+  return klo;
+}
+
+// One CTA per unit; its G heads are resolved concurrently by G warp groups
+// (named barriers), then the CTA compacts the group's final set.
+template <int G>
+__global__ void __launch_bounds__(kResThreads) topp_resolve_kernel(tw_paged_kv kv, tw_decode_params prm,
+                                                                    tw_decode_buffers buf) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  ResGroupSmem* GS = reinterpret_cast<ResGroupSmem*>(rsm);                 // [G]
+  uint32_t* keys = reinterpret_cast<uint32_t*>(rsm + G * sizeof(ResGroupSmem));  // [kMemberCap]
+  uint32_t* posn = keys + kMemberCap;                                        // [kMemberCap]
+  __shared__ TopHead R[G];
+  __shared__ int seg[G + 1], fill[G];
+  __shared__ uint32_t btmp[kResThreads / 32];
+  __shared__ int s_first;
+  const int unit = blockIdx.x, tid = threadIdx.x;
+  const size_t T = (size_t)kv.max_pages * kPage;
+  const int npos = buf.cand_count[unit] * kPage;
+  uint32_t* ubits = buf.sel_bits + (size_t)unit * (T / 32);
+  const uint64_t* mem = buf.topp_members + (size_t)unit * kMemberCap;
+  uint32_t* mcount = reinterpret_cast<uint32_t*>(buf.topp_ctr) + unit;
+  TT(2, 0);
+  if (tid < G) R[tid] = reinterpret_cast<const TopHead*>(buf.topp_heads)[(size_t)unit * G + tid];
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t acc = 0;
+    seg[0] = 0;
+    for (int g = 0; g < G; ++g) {
+      const bool in = R[g].cb >= 0 && acc + R[g].members <= (uint32_t)kMemberCap;
+      if (in) acc += R[g].members;
+      seg[g + 1] = acc;
+      fill[g] = 0;
+    }
+  }
+  __syncthreads();
+  // distribute the member list into per-head segments
+  const int m = (int)min(*mcount, (uint32_t)kMemberCap);
+  for (int i = tid; i < m; i += kResThreads) {
+    const uint64_t r = mem[i];
+    const int g = (int)(((uint32_t)r >> 24) & 0xFFu);
+    const int s = seg[g] + atomicAdd(&fill[g], 1);
+    keys[s] = (uint32_t)(r >> 32);
+    posn[s] = (uint32_t)r & 0xFFFFFFu;
+  }
+  __syncthreads();
+  TT(2, 1);
   {
-    const float zthr = thr == 0u ? -FLT_MAX : key2f(thr);  // thr = ~0 -> NaN: selects nothing
-    const float4* z4 = reinterpret_cast<const float4*>(z);
-    const int n4 = npos >> 2;
-    const int lane = threadIdx.x & 31;
-    for (int i0 = 0; i0 < n4; i0 += kTopThreads * kUnroll) {
-      float4 v[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int i = i0 + u * kTopThreads + threadIdx.x;
-        v[u] = i < n4 ? __ldcg(z4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    constexpr int kGT = kResThreads / G;
+    const int g = tid / kGT;
+    const Group grp{1 + g, kGT, tid % kGT};
+    ResGroupSmem& S = GS[g];
+    const TopHead& h = R[g];
+    const size_t qh = (size_t)unit * G + g;
+    uint32_t thr, sel_cnt = 0;
+    double sel_mass = 0.0;
+    if (h.cb == -2) {
+      thr = 0xFFFFFFFFu;
+    } else if (h.cb == -1) {
+      thr = 0u;
+      sel_cnt = h.b0;
+      sel_mass = h.Z;
+    } else {
+      uint32_t c = 0;
+      unsigned long long us = 0;
+      auto pick = [&](uint32_t k, uint32_t u, uint32_t pos) {
+        if (k >= thr) {
+          ++c;
+          us += u;
+          atomicOr(ubits + (pos >> 5), 1u << (pos & 31));
+        }
+      };
+      if (seg[g + 1] - seg[g] == (int)h.members && h.members > 0) {
+        const SmemSrc src{keys + seg[g], posn + seg[g], (int)h.members, h.M, h.cb};
+        thr = resolve_threshold(grp, src, h.above_mass, h.target, h.wb, S);
+        src.each(grp, pick);
+      } else {
+        const LogitSrc src{buf.logits + qh * T, npos, h.M, h.cb};
+        thr = resolve_threshold(grp, src, h.above_mass, h.target, h.wb, S);
+        src.each(grp, pick);
       }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int i = i0 + u * kTopThreads + threadIdx.x;
-        const uint32_t nib = (v[u].x >= zthr ? 1u : 0u) | (v[u].y >= zthr ? 2u : 0u) | (v[u].z >= zthr ? 4u : 0u) |
-                             (v[u].w >= zthr ? 8u : 0u);
-        uint32_t w = nib << (4 * (lane & 7));
-        w |= __shfl_xor_sync(0xffffffffu, w, 1);
-        w |= __shfl_xor_sync(0xffffffffu, w, 2);
-        w |= __shfl_xor_sync(0xffffffffu, w, 4);
-        if ((lane & 7) == 0 && i < n4) bits[i >> 3] = w;
-      }
+      uint32_t ct;
+      grp_scan<uint32_t>(grp, c, S.utmp, ct);
+      unsigned long long ut;
+      grp_scan<unsigned long long>(grp, us, S.ltmp, ut);
+      sel_cnt = h.above_cnt + ct;
+      sel_mass = h.above_mass + class_mass(h.wb, ct, ut);
+    }
+    if (grp.tid == 0) {
+      float* stats = buf.head_stats + qh * 4;
+      const bool empty = h.cb == -2;
+      buf.head_thr[qh] = thr;
+      stats[0] = (float)sel_cnt;
+      stats[1] = empty ? 0.f : (float)(sel_mass / h.Z);
+      stats[2] = empty || thr == 0u ? 0.f : (float)(exp((double)key2f(thr) - (double)h.M) / h.Z);
+      stats[3] = (float)h.b0;
     }
   }
-  if (threadIdx.x == 0) {
-    buf.head_thr[qh] = thr;
-    stats[0] = (float)sel_cnt;
-    stats[1] = empty ? 0.f : (float)(sel_mass / Z);
-    stats[2] = empty ? 0.f : (float)(exp((double)key2f(thr) - (double)M) / Z);
-    stats[3] = (float)b0;
-  }
-  TRACE("bitmap");
-  // ---- K3c: the last head of the unit forms the group set
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(buf.unit_done + unit, 1) == G - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
+  __syncthreads();  // member bits (global atomics of this CTA) are visible to its ld.cg below
+  TT(2, 2);
+  // ---- K3c: compact the union bitmap -> ascending token ids + attention work items
   const int* cand = buf.cand_pages + (size_t)unit * kv.max_pages;
   int* out = buf.final_idx + (size_t)unit * T;
   const int words = (npos + 31) >> 5;
-  const uint32_t* hb = buf.sel_bits + (size_t)unit * G * (T / 32);
-  uint32_t base = 0;
-  for (int w0 = 0; w0 < words; w0 += kTopThreads) {
-    const int w = w0 + threadIdx.x;
-    uint32_t x = 0;
-    if (w < words)
-      for (int g = 0; g < G; ++g) x |= __ldcg(hb + (size_t)g * (T / 32) + w);
-    // a word covers candidate pages 2w and 2w+1: fetch both page ids before the scan
-    const int c0 = x & 0xFFFFu ? cand[2 * w] * kPage : 0;
-    const int c1 = x >> 16 ? cand[2 * w + 1] * kPage - 16 : 0;
+  uint32_t basei = 0;
+  const int lane = tid & 31, warp = tid >> 5;
+  // the warp owns words w0 + 32 warp + j (j = lane) and their 64 candidate pages;
+  // the next block's words and pages are prefetched while this one is written
+  auto fetch = [&](int w0, uint32_t& x, int& pa, int& pb) {
+    const int w = w0 + tid;
+    x = w < words ? __ldcg(ubits + w) : 0u;
+    const int p0 = 2 * (w0 + 32 * warp);
+    pa = p0 + lane < kv.max_pages ? cand[p0 + lane] : 0;
+    pb = p0 + 32 + lane < kv.max_pages ? cand[p0 + 32 + lane] : 0;
+  };
+  uint32_t xn;
+  int pan, pbn;
+  fetch(0, xn, pan, pbn);
+  for (int w0 = 0; w0 < words; w0 += kResThreads) {
+    const uint32_t x = xn;
+    const int pa = pan, pb = pbn;
+    if (w0 + kResThreads < words) fetch(w0 + kResThreads, xn, pan, pbn);
     uint32_t total;
-    const uint32_t incl = cta_incl_scan<uint32_t>(__popc(x), S.utmp, total);
-    uint32_t pos = base + incl - __popc(x);
-    while (x) {
-      const int bit = __ffs(x) - 1;
-      x &= x - 1;
-      out[pos++] = (bit < 16 ? c0 : c1) + bit;
+    const uint32_t incl = block_incl_scan(__popc(x), btmp, total);
+    const uint32_t wbase = basei + incl - __popc(x);
+    // lane l writes bit l of each word: consecutive lanes -> consecutive ids (coalesced)
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t xw = __shfl_sync(0xffffffffu, x, j);
+      const uint32_t bw = __shfl_sync(0xffffffffu, wbase, j);
+      const int src = (2 * j + (lane >> 4)) & 31;
+      const int qa = __shfl_sync(0xffffffffu, pa, src), qb = __shfl_sync(0xffffffffu, pb, src);
+      if ((xw >> lane) & 1u)
+        out[bw + __popc(xw & ((1u << lane) - 1u))] = (j < 16 ? qa : qb) * kPage + (lane & 15);
     }
-    base += total;
+    basei += total;
   }
-  if (threadIdx.x == 0) {
-    buf.final_count[unit] = (int)base;
-    const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : TW_DEFAULT_CHUNK;
-    const int nitems = ((int)base + chunk - 1) / chunk;
-    const int first = nitems ? (int)atomicAdd(&buf.counters[0], (uint32_t)nitems) : 0;
-    buf.unit_items[2 * unit] = first;
+  TT(2, 3);
+  const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : TW_DEFAULT_CHUNK;
+  const int nitems = ((int)basei + chunk - 1) / chunk;
+  if (tid == 0) {
+    buf.final_count[unit] = (int)basei;
+    s_first = nitems ? (int)atomicAdd(&buf.counters[0], (uint32_t)nitems) : 0;
+    buf.unit_items[2 * unit] = s_first;
     buf.unit_items[2 * unit + 1] = nitems;
-    for (int i = 0; i < nitems; ++i) {
-      if (first + i < buf.max_items) {
-        buf.work_items[2 * (first + i)] = unit;
-        buf.work_items[2 * (first + i) + 1] = i * chunk;
-      }
+    *mcount = 0;
+  }
+  __syncthreads();
+  for (int i = tid; i < nitems; i += kResThreads) {
+    if (s_first + i < buf.max_items) {
+      buf.work_items[2 * (s_first + i)] = unit;
+      buf.work_items[2 * (s_first + i) + 1] = i * chunk;
     }
   }
+  TT(2, 4);
 }
 
 // ---------------------------------------------------------------- Algorithm 1, literally
@@ -571,27 +857,66 @@ __global__ void __launch_bounds__(256) topp_bisect_kernel(const double* __restri
 using namespace tw;
 
 #ifdef TW_TOPP_TRACE
-extern "C" int tw_debug_trace(unsigned long long* host_out) {
+extern "C" int tw_debug_ttrace(unsigned long long* host_out) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(host_out, g_trace, sizeof(g_trace));
-  int zeros[512] = {0};
-  cudaMemcpyToSymbol(g_trace_phase, zeros, sizeof(zeros));
+  cudaMemcpyFromSymbol(host_out, g_tt, sizeof(g_tt));
+  cudaMemset(host_out, 0, 0);
+  static unsigned long long zeros[3 * kTrCta * 8];
+  cudaMemcpyToSymbol(g_tt, zeros, sizeof(zeros));
   return 0;
 }
 #endif
 
+template <int G>
+static void launch_union(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,
+                         cudaStream_t stream) {
+  constexpr int kSlice = kUnionLogits / G;
+  const int T = kv->max_pages * kPage;
+  const int units = kv->num_seqs * kv->num_kv_heads;
+  topp_union_kernel<G><<<dim3((T + kSlice - 1) / kSlice, units), kTT, 0, stream>>>(*kv, *buf);
+  const int smem = G * (int)sizeof(ResGroupSmem) + 2 * kMemberCap * 4;
+  cudaFuncSetAttribute(topp_resolve_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  topp_resolve_kernel<G><<<units, kResThreads, smem, stream>>>(*kv, *prm, *buf);
+}
+
 extern "C" int tw_topp(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,
                        cudaStream_t stream) {
-  if (!kv || !prm || !buf || !buf->logits || !buf->head_thr || !buf->head_stats || !buf->final_idx ||
-      !buf->final_count || !buf->unit_items || !buf->work_items || !buf->counters)
+  if (!kv || !prm || !buf || !buf->logits || !buf->head_max || !buf->head_thr || !buf->head_stats ||
+      !buf->final_idx || !buf->final_count || !buf->unit_items || !buf->work_items || !buf->counters ||
+      !buf->sel_bits || !buf->topp_heads || !buf->topp_members ||
+      !buf->topp_ctr)
     return TW_ERR_INVALID;
   if (!(prm->p >= 0.0 && prm->p <= 1.0)) return TW_ERR_INVALID;
+  const long long T = (long long)kv->max_pages * kPage;
+  if (T > (1ll << 21)) return TW_ERR_INVALID;  // packed bin counts / member positions
   const int units = kv->num_seqs * kv->num_kv_heads;
-  if (!buf->sel_bits || !buf->unit_done) return TW_ERR_INVALID;
-  const size_t smem = sizeof(TopSmem);
-  cudaFuncSetAttribute(topp_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaMemsetAsync(buf->unit_done, 0, sizeof(int32_t) * units, stream);
-  topp_head_kernel<<<units * kv->group_size, kTopThreads, smem, stream>>>(*kv, *prm, *buf);
+  const int Hq = units * kv->group_size;
+  // histogram cluster: <= 8 CTAs (portable) of >= 8192 positions each
+  const int cs = (int)std::min<long long>(8, std::max<long long>(1, (T + kClusterLogits - 1) / kClusterLogits));
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs, Hq);
+    cfg.blockDim = dim3(kTT);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    tw_decode_params p = *prm;
+    tw_decode_buffers b = *buf;
+    tw_paged_kv k = *kv;
+    if (cudaLaunchKernelEx(&cfg, topp_hist_kernel, k, p, b) != cudaSuccess) return TW_ERR_CUDA;
+  }
+  switch (kv->group_size) {
+    case 1: launch_union<1>(kv, prm, buf, stream); break;
+    case 2: launch_union<2>(kv, prm, buf, stream); break;
+    case 4: launch_union<4>(kv, prm, buf, stream); break;
+    case 8: launch_union<8>(kv, prm, buf, stream); break;
+    default: return TW_ERR_INVALID;
+  }
   return launch_status();
 }
 

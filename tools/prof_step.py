@@ -40,7 +40,7 @@ for _ in range(args.reps):
     if args.dense:
         dec.dense(q, out)
 torch.cuda.synchronize()
-if os.environ.get("TW_LIB_PATH"):
+if os.environ.get("TW_LIB_PATH") and hasattr(__import__("paper_2502_02770_b200._lib", fromlist=["lib"]).lib(), "tw_debug_trace"):
     import ctypes
     import numpy as np
     from paper_2502_02770_b200 import _lib

@@ -1,5 +1,5 @@
 #!/bin/bash
-# build a traced copy of the library and print per-phase timestamps of topp_head_kernel
+# build a traced copy of the library (per-CTA phase timestamps of the top-p kernels)
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p /tmp/twtrace
