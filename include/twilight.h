@@ -39,8 +39,7 @@ extern "C" {
 #define TW_QBLOCK_BYTES 1152
 #define TW_DEFAULT_CHUNK 512 /* tokens per sparse-attention work item */
 #define TW_TOPP_BINS 4096        /* top-p histogram bins per query head */
-#define TW_TOPP_HEAD_BYTES 64    /* top-p per-head record */
-#define TW_TOPP_MEMBER_CAP 8192  /* crossing-bin members listed per unit (more: re-read path) */
+#define TW_TOPP_MEMBER_CAP 8192  /* crossing-bin members held on chip per unit (more: re-read path) */
 
 /* Status codes; the shim maps them to the reference's exceptions
  * (attention.py:30-36, pruner.py:67-76, quantcache.py:246-267). */
@@ -98,13 +97,9 @@ typedef struct tw_decode_buffers {
   uint32_t* counters;       /* [8]               device-side counters (zeroed by tw_select) */
   float* partials;          /* [max_items][G][d+2] split-KV partial (o[d], m, l) */
   uint32_t* head_page_bits; /* optional [Hq][ceil(max_pages/32)] per-head Quest page sets */
-  uint32_t* sel_bits;       /* [Hq][T/32]        per-head pruned set over candidate positions */
-  int32_t* unit_done;       /* [U]               completion counters (zero-initialised; left zeroed) */
+  uint32_t* sel_bits;       /* [U][T/32]         group-union bitmap over candidate positions */
   int32_t* band_idx;        /* [Hq][max_pages]   Quest pages in the fp32 filter's ambiguous band */
   double* band_scores;      /* [Hq][max_pages]   their exact fp64 bounds */
-  void* topp_heads;         /* [Hq][TW_TOPP_HEAD_BYTES] per-head crossing records */
-  uint64_t* topp_members;   /* [U][TW_TOPP_MEMBER_CAP] crossing-bin members (key, head, position) */
-  int32_t* topp_ctr;        /* [U]               member-list counts (zero-initialised; left zeroed) */
   int64_t max_items;
 } tw_decode_buffers;
 

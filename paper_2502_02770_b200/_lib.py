@@ -23,7 +23,6 @@ DEFAULT_CHUNK = 512
 QBLOCK_BYTES = 1152
 HEAD_DIM = 128
 TOPP_BINS = 4096          # TW_TOPP_BINS
-TOPP_HEAD_BYTES = 64      # TW_TOPP_HEAD_BYTES
 TOPP_MEMBER_CAP = 8192    # TW_TOPP_MEMBER_CAP
 
 # every symbol include/twilight.h declares
@@ -64,9 +63,8 @@ class TwDecodeBuffers(ctypes.Structure):
         ("head_stats", ctypes.c_void_p), ("final_idx", ctypes.c_void_p), ("final_count", ctypes.c_void_p),
         ("unit_items", ctypes.c_void_p), ("work_items", ctypes.c_void_p), ("counters", ctypes.c_void_p),
         ("partials", ctypes.c_void_p), ("head_page_bits", ctypes.c_void_p), ("sel_bits", ctypes.c_void_p),
-        ("unit_done", ctypes.c_void_p), ("band_idx", ctypes.c_void_p), ("band_scores", ctypes.c_void_p),
-        ("topp_heads", ctypes.c_void_p), ("topp_members", ctypes.c_void_p),
-        ("topp_ctr", ctypes.c_void_p), ("max_items", ctypes.c_int64),
+        ("band_idx", ctypes.c_void_p), ("band_scores", ctypes.c_void_p),
+        ("max_items", ctypes.c_int64),
     ]
 
 

@@ -6,66 +6,43 @@
 // runs until that set is the MINIMAL TIE-CLOSED top set whose mass reaches
 // p_eff = min(p, sum w) - 1e-9 (break rules :99-104).  We compute that set
 // directly instead of bisecting (~50 passes over the weights): a mass-weighted
-// radix select, split into two grid-wide kernels so that every pass over the
-// logits runs on the whole GPU (not one CTA per head):
+// radix select.  One CTA per unit (sequence, KV head) handles its G query
+// heads, with everything between the two reads of the logits on chip:
 //
-//   topp_hist   grid (head, 8192-logit chunk).  e_i = exp(z_i - max) is binned
-//               by (max - z) into 4096 bins of 1/120 logit; a bin holds
-//               (count, sum of u32 fixed-point deficits) packed in one u64, so
-//               bin masses are exact, order-independent integer sums (the
-//               result is deterministic).  Chunks merge into a per-head global
-//               histogram with u64 atomics; the head's last chunk CTA finds the
-//               crossing bin (first bin, highest z first, where the running mass
-//               reaches p_eff * Z) and writes the head record.
-//   topp_union  grid (unit, slice of candidate positions).  One read of the G
-//               heads' logits: a position is kept if, for some head, its bin
-//               lies above that head's crossing bin; crossing-bin members go to
-//               a per-unit list.  The unit's last slice CTA ranks each head's
-//               members exactly by fp32 logit key (key buckets, then an exact
-//               rank of <= 64 members; ties = equal logits = equal weights),
-//               adds them to the union bitmap, and compacts the group's final
-//               set (pipeline.py:347) into ascending token ids and attention
-//               work items.
+//   pass 1   e_i = exp(z_i - max) is binned by (max - z) into 4096 bins of
+//            1/120 logit per head (shared memory); a bin holds (count, sum of
+//            u32 fixed-point deficits), so bin masses are exact,
+//            order-independent integer sums (deterministic results).  The
+//            crossing bin of each head -- the first bin, highest z first,
+//            where the running mass reaches p_eff * Z -- is found by a scan
+//            (one warp group per head).
+//   pass 2   one read of the G heads' logits: a candidate position is kept if
+//            some head keeps it outright (bin above that head's crossing bin,
+//            a float compare against the bin's boundary); crossing-bin members
+//            are listed per head in shared memory.
+//   resolve  each head's members are ranked exactly by fp32 logit key (key
+//            buckets, then an exact rank of <= 64 members; ties = equal
+//            logits = equal weights); the union bitmap gets the members above
+//            the threshold, and the group's final set (pipeline.py:347) is
+//            compacted into ascending token ids and attention work items.
 //
-// The selected set is {z >= z_thr}: the reference's tie-closed set, up to
-// weights within ~1e-7 relative of the threshold (SFU exp inside a bin).
+// The histogram pass is bound by shared-memory atomic throughput (two per
+// logit); the rest is a few microseconds per unit.  The selected set is
+// {z >= z_thr}: the reference's tie-closed set, up to weights within ~1e-7
+// relative of the threshold (SFU exp inside a bin).
 #include <algorithm>
 #include <cfloat>
 
-#include <cooperative_groups.h>
-
 #include "block_scan.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace tw {
 
-#ifdef TW_TOPP_TRACE
-constexpr int kTrCta = 8192;
-__device__ unsigned long long g_tt[3][kTrCta][8];
-#define TT(k, ph)                                                                                    \
-  do {                                                                                               \
-    const int c_ = blockIdx.x + blockIdx.y * gridDim.x;                                              \
-    if (threadIdx.x == 0 && c_ < kTrCta) {                                                           \
-      unsigned long long now_;                                                                       \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));                                      \
-      g_tt[k][c_][ph] = now_;                                                                        \
-    }                                                                                                \
-  } while (0)
-#else
-#define TT(k, ph) do {} while (0)
-#endif
-
 constexpr int kBins = TW_TOPP_BINS;      // 4096
 constexpr float kBinPerLogit = 120.0f;   // bins cover (max - z) in [0, 34.1); the last bin takes the rest
-constexpr int kTT = 256;                 // threads of both kernels
-constexpr int kTW = kTT / 32;
-constexpr int kPerT = kBins / kTT;       // 16 bins per thread in the scans
-constexpr int kClusterLogits = 16384;    // candidate positions per histogram CTA (cluster size)
-constexpr int kUnionLogits = 16384;      // logits (positions x G) per union CTA
+constexpr int kHB = 4;                   // heads whose histograms are resident at once (4 x 32 KB)
 constexpr int kMemberCap = TW_TOPP_MEMBER_CAP;
-constexpr uint64_t kCntOne = 1ull << 43; // packed bin: count << 43 | deficit sum
-constexpr uint64_t kUsMask = kCntOne - 1;
+constexpr int kResBuckets = 1024;        // key buckets per refinement level
+constexpr int kRankCap = 64;             // members ranked exactly (O(k^2))
 constexpr float kUscale = 4194304.0f;    // deficits in units of 2^-22
 constexpr double kInvUscale = 1.0 / 4194304.0;
 // exp(-i/120), i = 0..15
@@ -73,20 +50,6 @@ __constant__ double kStepExp[16] = {
     1.0, 0.991701292638876, 0.9834714538216175, 0.9753099120283326, 0.9672161004820059, 0.9591894571091382,
     0.951229424500714, 0.9433354498734922, 0.9355069850316178, 0.9277434863285529, 0.9200444146293233,
     0.9124092352730778, 0.9048374180359595, 0.8973284370942841, 0.8898817709880238, 0.8824969025845955};
-
-// Per-head record written by topp_hist, read by topp_union.
-struct TopHead {
-  double above_mass;  // mass of the bins above the crossing bin
-  double target;      // p_eff * Z
-  double Z;           // total mass (in units of exp(z - max))
-  double wb;          // weight of the crossing bin's top, exp(t_cb - max)
-  int32_t cb;         // crossing bin; -1: keep every candidate; -2: keep nothing
-  uint32_t above_cnt, members, b0;
-  float M;            // max logit
-  float zhi, zlo;     // crossing bin = (zlo, zhi] in logit space: kept outright iff z > zhi
-  uint32_t pad;
-};
-static_assert(sizeof(TopHead) == TW_TOPP_HEAD_BYTES, "head record size");
 
 // Masses.  Bin b of (max - z) has top t_b = M - b/120 (float) and weight
 // w_b = exp(t_b - M) (fp64).  A member has e_i = exp(z_i - M) = w_b r_i with
@@ -106,7 +69,7 @@ __device__ __forceinline__ int dbin(float z, float M120) {
 __device__ __forceinline__ float bin_top(float M, int b) { return fmaf(-(float)b, 1.0f / kBinPerLogit, M); }
 // Largest float z with dbin(z) >= b (dbin is non-increasing in z), so bin b
 // is the float interval (bin_ceiling(b + 1), bin_ceiling(b)].
-__device__ float bin_ceiling(int b, float M, float M120) {
+__device__ __noinline__ float bin_ceiling(int b, float M, float M120) {
   if (b <= 0) return INFINITY;
   if (b >= kBins) return -INFINITY;
   float e = M - (float)b / kBinPerLogit;
@@ -127,343 +90,6 @@ __device__ __forceinline__ double class_mass(double w, uint64_t cnt, uint64_t us
 }
 __device__ __forceinline__ float4 ninf4() { return make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY); }
 __device__ __forceinline__ float comp(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
-
-// CTA-wide (kTT threads) inclusive scan.
-template <typename T>
-__device__ __forceinline__ T cta_scan(T v, T* tmp, T& total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  T x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const T y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) tmp[wid] = x;
-  __syncthreads();
-  T pre = T(0), tot = T(0);
-#pragma unroll
-  for (int i = 0; i < kTW; ++i) {
-    const T s = tmp[i];
-    pre += i < wid ? s : T(0);
-    tot += s;
-  }
-  __syncthreads();
-  total = tot;
-  return x + pre;
-}
-template <typename T>
-__device__ __forceinline__ T cta_sum(T v, T* tmp) {
-  T total;
-  cta_scan<T>(v, tmp, total);
-  return total;
-}
-
-struct ScanSmem {
-  double dtmp[kTW];
-  uint32_t utmp[kTW];
-  uint64_t ltmp[kTW];
-  int bin;
-  double above;
-  uint32_t above_cnt;
-};
-
-// First entry, in priority order (thread-major, then i), whose running mass
-// from `base` reaches `target`: -> S.bin (= rank, or -1), S.above, S.above_cnt.
-// `entry(i, m, c)` gives the mass and count of the thread's i-th entry (it is
-// evaluated twice instead of holding 16 doubles live).  Returns the total
-// mass; `ctot` receives the total count.
-template <class Entry>
-__device__ __forceinline__ double scan_crossing(Entry&& entry, double base, double target, bool target_is_fraction,
-                                                ScanSmem& S, uint32_t& ctot, double& target_out) {
-  double local = 0.0;
-  uint32_t lc = 0;
-#pragma unroll 4
-  for (int i = 0; i < kPerT; ++i) {
-    double m;
-    uint32_t c;
-    entry(i, m, c);
-    local += m;
-    lc += c;
-  }
-  double total;
-  const double incl = cta_scan<double>(local, S.dtmp, total);
-  const uint32_t cincl = cta_scan<uint32_t>(lc, S.utmp, ctot);
-  if (target_is_fraction) target *= total;
-  target_out = target;
-  if (threadIdx.x == 0) S.bin = -1;
-  __syncthreads();
-  const double excl = incl - local;
-  if (base + excl < target && target <= base + incl) {
-    double run = base + excl;
-    uint32_t crun = cincl - lc;
-#pragma unroll 1
-    for (int i = 0; i < kPerT; ++i) {
-      double m;
-      uint32_t c;
-      entry(i, m, c);
-      if (c && run + m >= target) {
-        S.bin = threadIdx.x * kPerT + i;
-        S.above = run;
-        S.above_cnt = crun;
-        break;
-      }
-      run += m;
-      crun += c;
-    }
-  }
-  __syncthreads();
-  return total;
-}
-
-// ---------------------------------------------------------------- K3b-1: histogram + crossing bin
-
-// grid (cluster size cs, Hq), cluster (cs, 1, 1): CTA `rank` of a head's
-// cluster bins positions [rank * chunk, (rank + 1) * chunk); the per-CTA bins
-// are merged through distributed shared memory (each rank sums a 1/cs slice of
-// the bins over the cluster into rank 0), and rank 0 finds the crossing bin.
-__global__ void __launch_bounds__(kTT, 4) topp_hist_kernel(tw_paged_kv kv, tw_decode_params prm, tw_decode_buffers buf) {
-  // per-CTA bins as two u32 arrays (native shared atomics; a u64 shared add
-  // is a CAS loop on sm_100a).  A regular bin's deficits are < 2^22/120 each;
-  // the deepest bin's (up to 2^22 each) go to a u64.
-  __shared__ uint32_t Hc[kBins], Hu[kBins];
-  __shared__ unsigned long long s_deep;
-  __shared__ ScanSmem S;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int cs = (int)cluster.num_blocks();
-  const int rank = (int)cluster.block_rank();
-  const int qh = blockIdx.y, tid = threadIdx.x;
-  const int unit = qh / kv.group_size;
-  const int npos = buf.cand_count[unit] * kPage;
-  TopHead* rec = reinterpret_cast<TopHead*>(buf.topp_heads) + qh;
-  const float M = key2f(buf.head_max[qh]);  // NaN when the head has no valid logit
-  const double p_eff = fmin(prm.p, 1.0) - 1e-9;
-  if (p_eff <= 0.0 || npos == 0 || !(M > -INFINITY)) {  // uniform over the cluster: nobody syncs
-    if (rank == 0 && tid == 0) {
-      TopHead r{};
-      r.cb = -2;
-      r.M = M;
-      r.zhi = r.zlo = INFINITY;
-      *rec = r;
-    }
-    return;
-  }
-  TT(0, 0);
-  const float M120 = M * kBinPerLogit;
-  for (int i = tid; i < kBins; i += kTT) Hc[i] = Hu[i] = 0;
-  if (tid == 0) s_deep = 0;
-  __syncthreads();
-  TT(0, 1);
-  {
-    const size_t T = (size_t)kv.max_pages * kPage;
-    const int chunk = ((npos + cs - 1) / cs + 1023) & ~1023;  // even split of the head's positions
-    const int lo = rank * chunk, hi = min(npos, lo + chunk);
-    const float4* z4 = reinterpret_cast<const float4*>(buf.logits + (size_t)qh * T);
-    unsigned long long deep = 0;
-    for (int p0 = lo; p0 < hi; p0 += 16 * kTT) {
-      float4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int p = p0 + 4 * (tid + u * kTT);
-        v[u] = p < hi ? __ldcg(z4 + (p >> 2)) : ninf4();
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float z = comp(v[u], e);
-          if (z > -INFINITY) {
-            const int b = dbin(z, M120);
-            const uint32_t d = deficit(z, M, b);
-            atomicAdd(&Hc[b], 1u);
-            if (b < kBins - 1) atomicAdd(&Hu[b], d);
-            else deep += d;
-          }
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) deep += __shfl_xor_sync(0xffffffffu, deep, o);
-    if ((tid & 31) == 0 && deep) atomicAdd(&s_deep, deep);
-  }
-  TT(0, 2);
-  if (cs > 1) {
-    cluster.sync();
-    TT(0, 3);
-    // rank r sums bins [r * 4096 / cs, (r + 1) * 4096 / cs) over the cluster into rank 0
-    const int per = kBins / cs;
-    const uint32_t* rc[8];
-    const uint32_t* ru[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      rc[r] = cluster.map_shared_rank(Hc, r < cs ? r : 0);
-      ru[r] = cluster.map_shared_rank(Hu, r < cs ? r : 0);
-    }
-    uint32_t* c0 = cluster.map_shared_rank(Hc, 0);
-    uint32_t* u0 = cluster.map_shared_rank(Hu, 0);
-    for (int i = rank * per + tid; i < (rank + 1) * per; i += kTT) {
-      uint32_t c[8], u[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        c[r] = r < cs ? rc[r][i] : 0u;
-        u[r] = r < cs ? ru[r][i] : 0u;
-      }
-      uint32_t cc = 0, uu = 0;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) { cc += c[r]; uu += u[r]; }
-      c0[i] = cc;
-      u0[i] = uu;
-    }
-    TT(0, 7);
-    if (rank == cs - 1 && tid == 0) {
-      unsigned long long d = 0;
-      for (int r = 0; r < cs; ++r) d += *cluster.map_shared_rank(&s_deep, r);
-      *cluster.map_shared_rank(&s_deep, 0) = d;
-    }
-    cluster.sync();
-    TT(0, 4);
-    if (rank != 0) return;
-  }
-  auto packed = [&](int i) -> uint64_t {
-    return ((uint64_t)Hc[i] << 43) | (i == kBins - 1 ? (uint64_t)s_deep : (uint64_t)Hu[i]);
-  };
-  // masses of this thread's 16 consecutive bins: one exp, then exact small steps
-  const int bfirst = tid * kPerT;
-  const float t0 = bin_top(M, bfirst);
-  const double w0 = exp((double)t0 - (double)M);
-  auto entry = [&](int i, double& m, uint32_t& c) {
-    const int bb = bfirst + i;
-    c = Hc[bb];
-    // exp(t_b - M) = w0 * exp(t_b - t0);  t_b - t0 = -i/120 + d (d ~ float rounding, tiny)
-    const double d = ((double)bin_top(M, bb) - (double)t0) + (double)i * (1.0 / 120.0);
-    const double w = w0 * kStepExp[i] * (1.0 + d * (1.0 + 0.5 * d));
-    m = c ? class_mass(w, c, packed(bb) & kUsMask) : 0.0;
-  };
-  uint32_t b0;
-  double target;
-  const double Z = scan_crossing(entry, 0.0, p_eff, true, S, b0, target);
-  TT(0, 6);
-  if (tid == 0) {
-    TopHead r{};
-    r.cb = S.bin;  // -1: rounding left the target above the total -> keep everything
-    r.above_mass = S.bin >= 0 ? S.above : 0.0;
-    r.above_cnt = S.bin >= 0 ? S.above_cnt : 0u;
-    r.members = S.bin >= 0 ? Hc[S.bin] : 0u;
-    r.b0 = b0;
-    r.Z = Z;
-    r.target = target;
-    r.wb = S.bin >= 0 ? exp((double)bin_top(M, S.bin) - (double)M) : 0.0;
-    r.M = M;
-    r.zhi = S.bin >= 0 ? bin_ceiling(S.bin, M, M120) : -INFINITY;
-    r.zlo = S.bin >= 0 ? bin_ceiling(S.bin + 1, M, M120) : -INFINITY;
-    *rec = r;
-  }
-  TT(0, 5);
-}
-
-// ---------------------------------------------------------------- K3b-2: union scan
-
-// One read of the G heads' logits over a slice of candidate positions: a
-// position is in the union bitmap if some head keeps it outright (bin above
-// the head's crossing bin); crossing-bin members are appended to the unit's
-// member list as (key << 32 | head << 24 | position).
-template <int G>
-__global__ void __launch_bounds__(kTT, 3) topp_union_kernel(tw_paged_kv kv, tw_decode_buffers buf) {
-  constexpr int kSlice = kUnionLogits / G;  // candidate positions per CTA
-  __shared__ float s_hi[G], s_lo[G];
-  const int unit = blockIdx.y, slice = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
-  const int npos = buf.cand_count[unit] * kPage;
-  const int base = slice * kSlice;
-  if (base >= npos) return;
-  TT(1, 0);
-  if (tid == 0) {
-    // heads whose crossing-bin members fit the unit's list (greedy, in head order); the
-    // others get an empty member range and are resolved by re-reading their logits
-    const TopHead* R = reinterpret_cast<const TopHead*>(buf.topp_heads) + (size_t)unit * G;
-    uint32_t acc = 0;
-    for (int g = 0; g < G; ++g) {
-      const bool in = R[g].cb >= 0 && acc + R[g].members <= (uint32_t)kMemberCap;
-      if (in) acc += R[g].members;
-      s_hi[g] = R[g].zhi;
-      s_lo[g] = in ? R[g].zlo : R[g].zhi;
-    }
-  }
-  __syncthreads();
-  float zhi[G], zlo[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) { zhi[g] = s_hi[g]; zlo[g] = s_lo[g]; }
-  const size_t T = (size_t)kv.max_pages * kPage;
-  const float* zu = buf.logits + (size_t)unit * G * T;
-  uint32_t* ubits = buf.sel_bits + (size_t)unit * (T / 32);
-  uint64_t* mem = buf.topp_members + (size_t)unit * kMemberCap;
-  uint32_t* mcount = reinterpret_cast<uint32_t*>(buf.topp_ctr) + unit;
-  const int len = min(kSlice, npos - base);
-  constexpr int kIters = kSlice / (4 * kTT);
-  float4 v[kIters][G];
-#pragma unroll
-  for (int it = 0; it < kIters; ++it) {
-    const int p0 = 4 * tid + it * 4 * kTT;
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-      v[it][g] = p0 < len ? __ldcg(reinterpret_cast<const float4*>(zu + g * T + base + p0)) : ninf4();
-  }
-  uint32_t nmem = 0;
-#pragma unroll
-  for (int it = 0; it < kIters; ++it) {
-    const int p0 = 4 * tid + it * 4 * kTT;
-    const int p = base + p0;
-    uint32_t nib = 0;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float z = comp(v[it][g], e);
-        nib |= (z > zhi[g] ? 1u : 0u) << e;
-        nmem += (z > zlo[g]) & (z <= zhi[g]);
-      }
-    }
-    uint32_t w = nib << (4 * (lane & 7));
-    w |= __shfl_xor_sync(0xffffffffu, w, 1);
-    w |= __shfl_xor_sync(0xffffffffu, w, 2);
-    w |= __shfl_xor_sync(0xffffffffu, w, 4);
-    if ((lane & 7) == 0 && p0 < len) ubits[p >> 5] = w;
-  }
-  TT(1, 1);
-  // crossing-bin members: one list reservation per CTA
-  __shared__ uint32_t s_tmp[kTT / 32];
-  __shared__ uint32_t s_base;
-  uint32_t total;
-  const uint32_t incl = cta_scan<uint32_t>(nmem, s_tmp, total);
-  if (total) {
-    if (tid == 0) s_base = atomicAdd(mcount, total);
-    __syncthreads();
-    TT(1, 2);
-    uint32_t slot = s_base + incl - nmem;
-    if (nmem) {
-#pragma unroll
-      for (int it = 0; it < kIters; ++it) {
-        const int p = base + 4 * tid + it * 4 * kTT;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float z = comp(v[it][g], e);
-            if (z > zlo[g] && z <= zhi[g]) {
-              if (slot < (uint32_t)kMemberCap)
-                mem[slot] = ((uint64_t)f2key(z) << 32) | ((uint64_t)g << 24) | (uint64_t)(p + e);
-              ++slot;
-            }
-          }
-        }
-      }
-    }
-  }
-  TT(1, 3);
-}
-
-// ---------------------------------------------------------------- K3b-3 / K3c: exact thresholds + group union
-
-constexpr int kResThreads = 512;
-constexpr int kResBuckets = 1024;  // key buckets per level
-constexpr int kRankCap = 64;       // members ranked exactly (O(k^2))
 
 template <typename T>
 __device__ __forceinline__ T grp_scan(const Group& g, T v, T* tmp, T& total) {
@@ -491,9 +117,9 @@ struct ResGroupSmem {
   uint32_t bc[kResBuckets];
   unsigned long long bu[kResBuckets];
   uint32_t rk[kRankCap], ru[kRankCap];
-  double dtmp[16];
-  uint32_t utmp[16];
-  unsigned long long ltmp[16];
+  double dtmp[32];
+  uint32_t utmp[32];
+  unsigned long long ltmp[32];
   uint32_t kmin, kmax, live, thr;
   int nr, bin;
   double above;
@@ -633,59 +259,248 @@ __device__ uint32_t resolve_threshold(const Group& g, const Src& src, double bas
   return klo;
 }
 
-// One CTA per unit; its G heads are resolved concurrently by G warp groups
-// (named barriers), then the CTA compacts the group's final set.
+
+// Per-head record (shared memory of the unit's CTA).
+struct HeadRec {
+  double above_mass;  // mass of the bins above the crossing bin
+  double target;      // p_eff * Z
+  double Z;           // total mass (in units of exp(z - max))
+  double wb;          // weight of the crossing bin's top, exp(t_cb - max)
+  int cb;             // crossing bin; -1: keep every candidate; -2: keep nothing
+  uint32_t above_cnt, members, b0;
+  float M;            // max logit
+  float zhi, zlo;     // crossing bin = (zlo, zhi]: kept outright iff z > zhi
+  int seg;            // member-list segment start (-1: resolved by re-reading the logits)
+};
+
 template <int G>
-__global__ void __launch_bounds__(kResThreads) topp_resolve_kernel(tw_paged_kv kv, tw_decode_params prm,
-                                                                    tw_decode_buffers buf) {
-  extern __shared__ __align__(16) unsigned char rsm[];
-  ResGroupSmem* GS = reinterpret_cast<ResGroupSmem*>(rsm);                 // [G]
-  uint32_t* keys = reinterpret_cast<uint32_t*>(rsm + G * sizeof(ResGroupSmem));  // [kMemberCap]
-  uint32_t* posn = keys + kMemberCap;                                        // [kMemberCap]
-  __shared__ TopHead R[G];
-  __shared__ int seg[G + 1], fill[G];
-  __shared__ uint32_t btmp[kResThreads / 32];
+struct UnitCfg {
+  static constexpr int GB = G < kHB ? G : kHB;  // heads per histogram batch
+  static constexpr int GT = G <= 2 ? 512 : 256;  // threads per head (warp group)
+  static constexpr int NT = GT * GB;            // threads
+  static constexpr size_t kHistBytes = (size_t)GB * kBins * 8;
+  static constexpr size_t kResBytes = (size_t)GB * sizeof(ResGroupSmem);
+  static constexpr size_t kSmem = (kHistBytes > kResBytes ? kHistBytes : kResBytes) + (size_t)kMemberCap * 8;
+};
+
+template <int G>
+__global__ void __launch_bounds__(UnitCfg<G>::NT) topp_unit_kernel(tw_paged_kv kv, tw_decode_params prm,
+                                                                  tw_decode_buffers buf) {
+  constexpr int GB = UnitCfg<G>::GB, NT = UnitCfg<G>::NT, kGT = UnitCfg<G>::GT;
+  constexpr int kPerT = kBins / kGT;  // bins per thread in the crossing scan
+  extern __shared__ __align__(16) unsigned char sm[];
+  uint32_t* Hc = reinterpret_cast<uint32_t*>(sm);                           // [GB][kBins] counts
+  uint32_t* Hu = Hc + GB * kBins;                                            // [GB][kBins] deficit sums
+  ResGroupSmem* RS = reinterpret_cast<ResGroupSmem*>(sm);                    // [GB] (aliases the bins)
+  uint32_t* mkey = reinterpret_cast<uint32_t*>(sm + UnitCfg<G>::kSmem - (size_t)kMemberCap * 8);  // [cap]
+  uint32_t* mpos = mkey + kMemberCap;                                        // [cap]
+  __shared__ HeadRec R[G];
+  __shared__ unsigned long long s_deep[GB];
+  __shared__ int s_fill[G];
+  __shared__ uint32_t btmp[NT / 32];
   __shared__ int s_first;
-  const int unit = blockIdx.x, tid = threadIdx.x;
+  const int unit = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gp = tid / kGT;
+  const Group grp{1 + gp, kGT, tid % kGT};
   const size_t T = (size_t)kv.max_pages * kPage;
   const int npos = buf.cand_count[unit] * kPage;
+  const int n4 = npos >> 2;
+  const float* zu = buf.logits + (size_t)unit * G * T;
   uint32_t* ubits = buf.sel_bits + (size_t)unit * (T / 32);
-  const uint64_t* mem = buf.topp_members + (size_t)unit * kMemberCap;
-  uint32_t* mcount = reinterpret_cast<uint32_t*>(buf.topp_ctr) + unit;
-  TT(2, 0);
-  if (tid < G) R[tid] = reinterpret_cast<const TopHead*>(buf.topp_heads)[(size_t)unit * G + tid];
+  const double p_eff = fmin(prm.p, 1.0) - 1e-9;
+  if (tid < G) {
+    const float M = key2f(buf.head_max[(size_t)unit * G + tid]);  // NaN when the head has no valid logit
+    HeadRec r{};
+    r.M = M;
+    r.cb = (p_eff <= 0.0 || npos == 0 || !(M > -INFINITY)) ? -2 : 0;
+    r.zhi = r.zlo = INFINITY;
+    r.seg = -1;
+    R[tid] = r;
+    s_fill[tid] = 0;
+  }
   __syncthreads();
+
+  // ---- pass 1 (per batch of GB heads): bins, then each head's crossing bin
+#pragma unroll 1
+  for (int g0 = 0; g0 < G; g0 += GB) {
+    for (int i = tid; i < GB * kBins; i += NT) Hc[i] = Hu[i] = 0;
+    if (tid < GB) s_deep[tid] = 0;
+    __syncthreads();
+    {
+      float Mh[GB], m120[GB];
+      bool act[GB];
+      unsigned long long deep[GB];
+#pragma unroll
+      for (int h = 0; h < GB; ++h) {
+        act[h] = g0 + h < G && R[g0 + h].cb != -2;
+        Mh[h] = act[h] ? R[g0 + h].M : 0.f;
+        m120[h] = Mh[h] * kBinPerLogit;
+        deep[h] = 0;
+      }
+#pragma unroll 2
+      for (int i = tid; i < n4; i += NT) {
+        float4 v[GB];
+#pragma unroll
+        for (int h = 0; h < GB; ++h)
+          v[h] = act[h] ? __ldcg(reinterpret_cast<const float4*>(zu + (size_t)(g0 + h) * T) + i) : ninf4();
+#pragma unroll
+        for (int h = 0; h < GB; ++h)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float z = comp(v[h], e);
+            if (z > -INFINITY) {
+              const int b = dbin(z, m120[h]);
+              const uint32_t d = deficit(z, Mh[h], b);
+              atomicAdd(&Hc[h * kBins + b], 1u);
+              if (b < kBins - 1) atomicAdd(&Hu[h * kBins + b], d);
+              else deep[h] += d;  // the deepest bin's deficits (up to 2^22 each) need 64 bits
+            }
+          }
+      }
+#pragma unroll
+      for (int h = 0; h < GB; ++h) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) deep[h] += __shfl_xor_sync(0xffffffffu, deep[h], o);
+        if (lane == 0 && deep[h]) atomicAdd(&s_deep[h], deep[h]);
+      }
+    }
+    __syncthreads();
+    const int g = g0 + gp;
+    if (g < G && R[g].cb != -2) {  // uniform per warp group
+      const uint32_t* hc = Hc + gp * kBins;
+      const uint32_t* hu = Hu + gp * kBins;
+      const float M = R[g].M;
+      const float M120 = M * kBinPerLogit;
+      const int bfirst = grp.tid * kPerT;
+      const float t0 = bin_top(M, bfirst);
+      const double w0 = exp((double)t0 - (double)M);
+      auto mass = [&](int i, uint32_t& c) -> double {
+        const int bb = bfirst + i;
+        c = hc[bb];
+        if (!c) return 0.0;
+        const uint64_t us = bb == kBins - 1 ? (uint64_t)s_deep[gp] : (uint64_t)hu[bb];
+        // exp(t_b - M) = w0 * exp(t_b - t0);  t_b - t0 = -i/120 + d (d ~ float rounding, tiny)
+        const double d = ((double)bin_top(M, bb) - (double)t0) + (double)i * (1.0 / 120.0);
+        return class_mass(w0 * kStepExp[i] * (1.0 + d * (1.0 + 0.5 * d)), c, us);
+      };
+      static_assert(kPerT <= 16, "kStepExp covers 16 bins per thread");
+      double local = 0.0;
+      uint32_t lc = 0;
+#pragma unroll 4
+      for (int i = 0; i < kPerT; ++i) {
+        uint32_t c;
+        local += mass(i, c);
+        lc += c;
+      }
+      double Z;
+      uint32_t b0;
+      __shared__ double s_dtmp[GB][kGT / 32];
+      __shared__ uint32_t s_utmp[GB][kGT / 32];
+      __shared__ int s_bin[GB];
+      __shared__ double s_above[GB];
+      __shared__ uint32_t s_acnt[GB];
+      const double incl = grp_scan<double>(grp, local, s_dtmp[gp], Z);
+      const uint32_t cincl = grp_scan<uint32_t>(grp, lc, s_utmp[gp], b0);
+      const double target = p_eff * Z;
+      if (grp.tid == 0) s_bin[gp] = -1;
+      grp.sync();
+      const double excl = incl - local;
+      if (excl < target && target <= incl) {
+        double run = excl;
+        uint32_t crun = cincl - lc;
+#pragma unroll 1
+        for (int i = 0; i < kPerT; ++i) {
+          uint32_t c;
+          const double m = mass(i, c);
+          if (c && run + m >= target) {
+            s_bin[gp] = bfirst + i;
+            s_above[gp] = run;
+            s_acnt[gp] = crun;
+            break;
+          }
+          run += m;
+          crun += c;
+        }
+      }
+      grp.sync();
+      if (grp.tid == 0) {
+        HeadRec& r = R[g];
+        const int cb = s_bin[gp];  // -1: rounding left the target above the total -> keep everything
+        r.cb = cb;
+        r.Z = Z;
+        r.target = target;
+        r.b0 = b0;
+        if (cb >= 0) {
+          r.above_mass = s_above[gp];
+          r.above_cnt = s_acnt[gp];
+          r.members = hc[cb];
+          r.wb = exp((double)bin_top(M, cb) - (double)M);
+          r.zhi = bin_ceiling(cb, M, M120);
+          r.zlo = bin_ceiling(cb + 1, M, M120);
+        } else {
+          r.zhi = r.zlo = -INFINITY;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // member-list segments: heads in order while they fit; the rest re-read their logits
   if (tid == 0) {
     uint32_t acc = 0;
-    seg[0] = 0;
     for (int g = 0; g < G; ++g) {
-      const bool in = R[g].cb >= 0 && acc + R[g].members <= (uint32_t)kMemberCap;
-      if (in) acc += R[g].members;
-      seg[g + 1] = acc;
-      fill[g] = 0;
+      HeadRec& r = R[g];
+      if (r.cb >= 0 && acc + r.members <= (uint32_t)kMemberCap) {
+        r.seg = (int)acc;
+        acc += r.members;
+      } else if (r.cb >= 0) {
+        r.zlo = r.zhi;  // empty member range in pass 2
+      }
     }
   }
   __syncthreads();
-  // distribute the member list into per-head segments
-  const int m = (int)min(*mcount, (uint32_t)kMemberCap);
-  for (int i = tid; i < m; i += kResThreads) {
-    const uint64_t r = mem[i];
-    const int g = (int)(((uint32_t)r >> 24) & 0xFFu);
-    const int s = seg[g] + atomicAdd(&fill[g], 1);
-    keys[s] = (uint32_t)(r >> 32);
-    posn[s] = (uint32_t)r & 0xFFFFFFu;
+
+  // ---- pass 2: union of the heads' outright-kept positions + crossing-bin members
+  {
+    float zhi[G], zlo[G];
+    int sg[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) { zhi[g] = R[g].zhi; zlo[g] = R[g].zlo; sg[g] = R[g].seg; }
+#pragma unroll 2
+    for (int i0 = 0; i0 < n4; i0 += NT) {
+      const int i = i0 + tid;
+      const bool valid = i < n4;
+      uint32_t nib = 0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float4 v = valid ? __ldcg(reinterpret_cast<const float4*>(zu + (size_t)g * T) + i) : ninf4();
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float z = comp(v, e);
+          nib |= (z > zhi[g] ? 1u : 0u) << e;
+          if (z > zlo[g] && z <= zhi[g]) {
+            const int s = sg[g] + atomicAdd(&s_fill[g], 1);
+            mkey[s] = f2key(z);
+            mpos[s] = (uint32_t)(4 * i + e);
+          }
+        }
+      }
+      uint32_t w = nib << (4 * (lane & 7));
+      w |= __shfl_xor_sync(0xffffffffu, w, 1);
+      w |= __shfl_xor_sync(0xffffffffu, w, 2);
+      w |= __shfl_xor_sync(0xffffffffu, w, 4);
+      if ((lane & 7) == 0 && valid) ubits[i >> 3] = w;
+    }
   }
   __syncthreads();
-  TT(2, 1);
-  {
-    constexpr int kGT = kResThreads / G;
-    const int g = tid / kGT;
-    const Group grp{1 + g, kGT, tid % kGT};
-    ResGroupSmem& S = GS[g];
-    const TopHead& h = R[g];
+
+  // ---- resolve: exact threshold class inside each head's crossing bin (warp group per head)
+#pragma unroll 1
+  for (int g = gp; g < G; g += GB) {
+    const HeadRec& h = R[g];
     const size_t qh = (size_t)unit * G + g;
     uint32_t thr, sel_cnt = 0;
     double sel_mass = 0.0;
+    ResGroupSmem& S = RS[gp];
     if (h.cb == -2) {
       thr = 0xFFFFFFFFu;
     } else if (h.cb == -1) {
@@ -702,12 +517,12 @@ __global__ void __launch_bounds__(kResThreads) topp_resolve_kernel(tw_paged_kv k
           atomicOr(ubits + (pos >> 5), 1u << (pos & 31));
         }
       };
-      if (seg[g + 1] - seg[g] == (int)h.members && h.members > 0) {
-        const SmemSrc src{keys + seg[g], posn + seg[g], (int)h.members, h.M, h.cb};
+      if (h.seg >= 0) {
+        const SmemSrc src{mkey + h.seg, mpos + h.seg, (int)h.members, h.M, h.cb};
         thr = resolve_threshold(grp, src, h.above_mass, h.target, h.wb, S);
         src.each(grp, pick);
       } else {
-        const LogitSrc src{buf.logits + qh * T, npos, h.M, h.cb};
+        const LogitSrc src{zu + (size_t)g * T, npos, h.M, h.cb};
         thr = resolve_threshold(grp, src, h.above_mass, h.target, h.wb, S);
         src.each(grp, pick);
       }
@@ -727,15 +542,15 @@ __global__ void __launch_bounds__(kResThreads) topp_resolve_kernel(tw_paged_kv k
       stats[2] = empty || thr == 0u ? 0.f : (float)(exp((double)key2f(thr) - (double)h.M) / h.Z);
       stats[3] = (float)h.b0;
     }
+    grp.sync();
   }
   __syncthreads();  // member bits (global atomics of this CTA) are visible to its ld.cg below
-  TT(2, 2);
+
   // ---- K3c: compact the union bitmap -> ascending token ids + attention work items
   const int* cand = buf.cand_pages + (size_t)unit * kv.max_pages;
   int* out = buf.final_idx + (size_t)unit * T;
   const int words = (npos + 31) >> 5;
   uint32_t basei = 0;
-  const int lane = tid & 31, warp = tid >> 5;
   // the warp owns words w0 + 32 warp + j (j = lane) and their 64 candidate pages;
   // the next block's words and pages are prefetched while this one is written
   auto fetch = [&](int w0, uint32_t& x, int& pa, int& pb) {
@@ -748,10 +563,10 @@ __global__ void __launch_bounds__(kResThreads) topp_resolve_kernel(tw_paged_kv k
   uint32_t xn;
   int pan, pbn;
   fetch(0, xn, pan, pbn);
-  for (int w0 = 0; w0 < words; w0 += kResThreads) {
+  for (int w0 = 0; w0 < words; w0 += NT) {
     const uint32_t x = xn;
     const int pa = pan, pb = pbn;
-    if (w0 + kResThreads < words) fetch(w0 + kResThreads, xn, pan, pbn);
+    if (w0 + NT < words) fetch(w0 + NT, xn, pan, pbn);
     uint32_t total;
     const uint32_t incl = block_incl_scan(__popc(x), btmp, total);
     const uint32_t wbase = basei + incl - __popc(x);
@@ -767,7 +582,6 @@ __global__ void __launch_bounds__(kResThreads) topp_resolve_kernel(tw_paged_kv k
     }
     basei += total;
   }
-  TT(2, 3);
   const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : TW_DEFAULT_CHUNK;
   const int nitems = ((int)basei + chunk - 1) / chunk;
   if (tid == 0) {
@@ -775,16 +589,14 @@ __global__ void __launch_bounds__(kResThreads) topp_resolve_kernel(tw_paged_kv k
     s_first = nitems ? (int)atomicAdd(&buf.counters[0], (uint32_t)nitems) : 0;
     buf.unit_items[2 * unit] = s_first;
     buf.unit_items[2 * unit + 1] = nitems;
-    *mcount = 0;
   }
   __syncthreads();
-  for (int i = tid; i < nitems; i += kResThreads) {
+  for (int i = tid; i < nitems; i += NT) {
     if (s_first + i < buf.max_items) {
       buf.work_items[2 * (s_first + i)] = unit;
       buf.work_items[2 * (s_first + i) + 1] = i * chunk;
     }
   }
-  TT(2, 4);
 }
 
 // ---------------------------------------------------------------- Algorithm 1, literally
@@ -856,68 +668,33 @@ __global__ void __launch_bounds__(256) topp_bisect_kernel(const double* __restri
 
 using namespace tw;
 
-#ifdef TW_TOPP_TRACE
-extern "C" int tw_debug_ttrace(unsigned long long* host_out) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(host_out, g_tt, sizeof(g_tt));
-  cudaMemset(host_out, 0, 0);
-  static unsigned long long zeros[3 * kTrCta * 8];
-  cudaMemcpyToSymbol(g_tt, zeros, sizeof(zeros));
-  return 0;
-}
-#endif
-
 template <int G>
-static void launch_union(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,
-                         cudaStream_t stream) {
-  constexpr int kSlice = kUnionLogits / G;
-  const int T = kv->max_pages * kPage;
-  const int units = kv->num_seqs * kv->num_kv_heads;
-  topp_union_kernel<G><<<dim3((T + kSlice - 1) / kSlice, units), kTT, 0, stream>>>(*kv, *buf);
-  const int smem = G * (int)sizeof(ResGroupSmem) + 2 * kMemberCap * 4;
-  cudaFuncSetAttribute(topp_resolve_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  topp_resolve_kernel<G><<<units, kResThreads, smem, stream>>>(*kv, *prm, *buf);
+static int launch_unit(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,
+                       cudaStream_t stream) {
+  const size_t smem = UnitCfg<G>::kSmem;
+  if (cudaFuncSetAttribute(topp_unit_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return TW_ERR_CUDA;
+  topp_unit_kernel<G><<<kv->num_seqs * kv->num_kv_heads, UnitCfg<G>::NT, smem, stream>>>(*kv, *prm, *buf);
+  return launch_status();
 }
 
 extern "C" int tw_topp(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,
                        cudaStream_t stream) {
   if (!kv || !prm || !buf || !buf->logits || !buf->head_max || !buf->head_thr || !buf->head_stats ||
       !buf->final_idx || !buf->final_count || !buf->unit_items || !buf->work_items || !buf->counters ||
-      !buf->sel_bits || !buf->topp_heads || !buf->topp_members ||
-      !buf->topp_ctr)
+      !buf->sel_bits)
     return TW_ERR_INVALID;
   if (!(prm->p >= 0.0 && prm->p <= 1.0)) return TW_ERR_INVALID;
   const long long T = (long long)kv->max_pages * kPage;
-  if (T > (1ll << 21)) return TW_ERR_INVALID;  // packed bin counts / member positions
-  const int units = kv->num_seqs * kv->num_kv_heads;
-  const int Hq = units * kv->group_size;
-  // histogram cluster: <= 8 CTAs (portable) of >= 8192 positions each
-  const int cs = (int)std::min<long long>(8, std::max<long long>(1, (T + kClusterLogits - 1) / kClusterLogits));
-  {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs, Hq);
-    cfg.blockDim = dim3(kTT);
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cs;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    tw_decode_params p = *prm;
-    tw_decode_buffers b = *buf;
-    tw_paged_kv k = *kv;
-    if (cudaLaunchKernelEx(&cfg, topp_hist_kernel, k, p, b) != cudaSuccess) return TW_ERR_CUDA;
-  }
+  if (T > (1ll << 24)) return TW_ERR_INVALID;  // member positions are 24-bit
   switch (kv->group_size) {
-    case 1: launch_union<1>(kv, prm, buf, stream); break;
-    case 2: launch_union<2>(kv, prm, buf, stream); break;
-    case 4: launch_union<4>(kv, prm, buf, stream); break;
-    case 8: launch_union<8>(kv, prm, buf, stream); break;
+    case 1: return launch_unit<1>(kv, prm, buf, stream);
+    case 2: return launch_unit<2>(kv, prm, buf, stream);
+    case 4: return launch_unit<4>(kv, prm, buf, stream);
+    case 8: return launch_unit<8>(kv, prm, buf, stream);
     default: return TW_ERR_INVALID;
   }
-  return launch_status();
 }
 
 extern "C" int tw_topp_bisect(const double* weights, int32_t rows, int32_t n, double p, double epsilon,

@@ -200,19 +200,13 @@ class DecodeBuffers:
         self.partials = torch.empty(self.max_items, G, L.HEAD_DIM + 2, dtype=torch.float32, device=dev)
         words = -(-cache.max_pages // 32)
         self.head_page_bits = torch.zeros(Hq, words, dtype=torch.int32, device=dev) if head_page_bits else None
-        self.sel_bits = torch.zeros(Hq, T // 32, dtype=torch.int32, device=dev)
-        self.unit_done = torch.zeros(U, dtype=torch.int32, device=dev)
+        self.sel_bits = torch.zeros(U, T // 32, dtype=torch.int32, device=dev)
         self.band_idx = torch.empty(Hq, cache.max_pages, dtype=torch.int32, device=dev)
         self.band_scores = torch.empty(Hq, cache.max_pages, dtype=torch.float64, device=dev)
-        # top-p scratch: the library leaves the member counters zeroed after every step
-        self.topp_heads = torch.zeros(Hq, L.TOPP_HEAD_BYTES, dtype=torch.uint8, device=dev)
-        self.topp_members = torch.empty(U, L.TOPP_MEMBER_CAP, dtype=torch.int64, device=dev)
-        self.topp_ctr = torch.zeros(U, dtype=torch.int32, device=dev)
         s = L.TwDecodeBuffers()
         for name in ("page_scores", "cand_pages", "cand_count", "logits", "head_max", "head_thr", "head_stats",
                      "final_idx", "final_count", "unit_items", "work_items", "counters", "partials",
-                     "head_page_bits", "sel_bits", "unit_done", "band_idx", "band_scores", "topp_heads",
-                     "topp_members", "topp_ctr"):
+                     "head_page_bits", "sel_bits", "band_idx", "band_scores"):
             setattr(s, name, L.ptr(getattr(self, name)))
         s.max_items = self.max_items
         self._struct = s
