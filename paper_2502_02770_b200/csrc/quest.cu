@@ -144,7 +144,10 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_kernel(tw_paged_kv
 // (bf16 products exact, fp32 accumulation, covered by the select margin).
 // Per warp: 16-page tiles (16 x 512 B, XOR-swizzled rows) through a 3-stage
 // cp.async ring; one ldmatrix.x4 + one MMA per page-tile k-step.
-constexpr int kQmStages = 3;
+#ifndef TW_QM_STAGES
+#define TW_QM_STAGES 3
+#endif
+constexpr int kQmStages = TW_QM_STAGES;
 
 __device__ __forceinline__ void ldsm_x4_q(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"

@@ -1,16 +1,20 @@
 #!/bin/bash
-# One profiling pass for profiles/: launch list (per-kernel device time + DRAM
-# bytes, serialized/cold) and an ncu --set full capture of the hot kernels.
-# usage (on the GPU box): tools/profile_round.sh <tag> [config]
+# One profiling pass for profiles/ (run on the GPU box):  tools/profile_round.sh <tag>
+#   bench lines (ours, reference arm, other configs), the launch list of the bench
+#   command (ncu gpu__time_duration, cold/serialised), one ncu --set full capture of
+#   the step's kernels (summary + per-stage DRAM traffic), GPU tests.
 set -u
 TAG=${1:-r01}
-CFG=${2:-C2}
 mkdir -p gpurun_out
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-  --csv --log-file gpurun_out/launches_${TAG}_${CFG}.csv python tools/prof_step.py --config $CFG --reps 2 > /dev/null 2>&1
-python tools/launches.py gpurun_out/launches_${TAG}_${CFG}.csv --json gpurun_out/launches_${TAG}_${CFG}.json | grep "tw::" || true
+python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 900 python bench.py > gpurun_out/bench_${TAG}_C2.json 2> gpurun_out/bench_${TAG}_C2.err; tail -c 400 gpurun_out/bench_${TAG}_C2.json
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_${TAG}_C2.json 2>&1; tail -c 300 gpurun_out/bench_ref_${TAG}_C2.json
+for c in C1 C3 C5; do timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_${TAG}_$c.json 2> gpurun_out/bench_${TAG}_$c.err; done
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/launches_${TAG}_C2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+python tools/launches.py gpurun_out/launches_${TAG}_C2.csv --json gpurun_out/launches_${TAG}_C2.json | grep "tw::" || true
 timeout 900 ncu --set full --import-source on --clock-control none \
-  -k regex:"attn_kernel|quest_select|topp_head|estimate_kernel|quest_filter|append_kernel|merge_kernel" -c 8 \
-  -o gpurun_out/full_${TAG}_${CFG} python tools/prof_step.py --config $CFG --reps 1 > /dev/null 2>&1
-python tools/ncu_hot.py gpurun_out/full_${TAG}_${CFG}.ncu-rep . --lines 6 > gpurun_out/full_${TAG}_${CFG}.txt 2>&1
-cat gpurun_out/full_${TAG}_${CFG}.txt | grep -E "^==|time|stalls"
+  -k regex:"attn_kernel|quest_select|topp_unit|estimate_kernel|quest_filter|append_kernel|merge_kernel" -c 8 \
+  -o gpurun_out/full_${TAG}_C2 python tools/prof_step.py --config C2 --reps 1 > /dev/null 2>&1
+python tools/ncu_hot.py gpurun_out/full_${TAG}_C2.ncu-rep . --lines 6 > gpurun_out/ncu_full_${TAG}_C2.txt 2>&1
+python tools/traffic_json.py gpurun_out/full_${TAG}_C2.ncu-rep C2 > gpurun_out/traffic_${TAG}_C2.json 2>&1 || true

@@ -14,7 +14,7 @@ STAGES = {
     "K1_append": ["append_kernel"],
     "K2_select": ["quest_filter", "quest_select"],
     "K3a_estimate": ["estimate_kernel"],
-    "K3bc_topp": ["topp_head"],
+    "K3bc_topp": ["topp_unit"],
     "K4_attention": ["attn_kernel", "merge_kernel"],
 }
 
