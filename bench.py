@@ -55,6 +55,18 @@ TAUS = (0.25, 0.5, 1.0, 2.0)  # per-KV-head temperatures, cycled: focused .. dif
 METRIC = "sparse decode-attn us/layer & achieved HBM GB/s at 32k-128k ctx, 1/2/4/8 GPU"
 
 
+def load_read_peak():
+    """Read-only streaming bandwidth measured by tools/microbench.cu on a B200
+    (profiles/microbench_r01.json): the attention/estimate kernels only read,
+    and a read stream runs above the copy (read+write) figure."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "microbench_r01.json")) as f:
+            d = json.load(f)
+        return max(v for k, v in d.items() if k.startswith("stream_read_gbs"))
+    except Exception:
+        return None
+
+
 def load_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -406,11 +418,14 @@ def run_ours(args, cfg):
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us/layer", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "path": "tw_decode_step C-ABI call (captured), q/k_new/v_new from pinned host, out to pinned host"},
-        "gpu_launches": (8 if cfg["selector"] == "quest" else 7) * args.steps,
+        "gpu_launches": (7 if cfg["selector"] == "quest" else 6) * args.steps,  # append, [filter], select, estimate, top-p, attention, merge
         "roofline": {"bound": "hbm", "kernel": dominant,
                      "achieved": round(kernel_gbs[dominant], 1) if kernel_gbs[dominant] else None,
                      "peak": peak, "unit": "GB/s",
                      "frac": round(kernel_gbs[dominant] / peak, 4) if kernel_gbs[dominant] else None,
+                     "read_peak": load_read_peak(),
+                     "frac_vs_read_peak": (round(kernel_gbs[dominant] / load_read_peak(), 4)
+                                           if kernel_gbs[dominant] and load_read_peak() else None),
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": ab[dominant]},
         "step_roofline": {"algorithmic_bytes": ab["step"], "achieved_gbs_per_gpu": round(achieved_step, 1),
@@ -578,6 +593,9 @@ def run_model(args, cfg):
                      "achieved": round(kernel_gbs[dominant], 1) if kernel_gbs[dominant] else None,
                      "peak": peak, "unit": "GB/s",
                      "frac": round(kernel_gbs[dominant] / peak, 4) if kernel_gbs[dominant] else None,
+                     "read_peak": load_read_peak(),
+                     "frac_vs_read_peak": (round(kernel_gbs[dominant] / load_read_peak(), 4)
+                                           if kernel_gbs[dominant] and load_read_peak() else None),
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": ab[dominant]},
         "step_roofline": {"algorithmic_bytes": step_bytes, "weights_bytes": wbytes,

@@ -87,7 +87,7 @@ typedef struct tw_decode_buffers {
   int32_t* cand_pages;      /* [U][max_pages]    sorted candidate logical pages (group union) */
   int32_t* cand_count;      /* [U] */
   float* logits;            /* [U][G][T]         INT4-estimated logits, -inf past seq end */
-  uint32_t* head_max;       /* [Hq]              max logit (ordered key) */
+  uint32_t* head_max;       /* [Hq]              max logit (ordered key); zeroed by tw_select */
   uint32_t* head_thr;       /* [Hq]              top-p threshold (ordered key of the logit) */
   float* head_stats;        /* [Hq][4]           B1, candidate mass, threshold weight, B0 */
   int32_t* final_idx;       /* [U][T]            group-shared surviving token ids, ascending */

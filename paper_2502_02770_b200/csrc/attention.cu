@@ -28,7 +28,10 @@ namespace tw {
 constexpr int kAttWarps = 4;            // warps (= independent workers) per CTA
 constexpr int kAttThreads = kAttWarps * 32;
 constexpr int kTile = 16;               // rows per stage
-constexpr int kNS = 3;                  // stages per warp
+#ifndef TW_ATT_STAGES
+#define TW_ATT_STAGES 3
+#endif
+constexpr int kNS = TW_ATT_STAGES;      // stages per warp
 constexpr int kMaxChunk = 512;          // tokens per work item (upper bound)
 constexpr int kDefaultChunk = TW_DEFAULT_CHUNK;
 constexpr int kDenseChunk = 512;
@@ -226,6 +229,8 @@ template <typename T, int G, bool DENSE>
 __global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const T* __restrict__ q,
                                                            tw_decode_buffers buf, float* __restrict__ out,
                                                            int chunk, int max_chunks, int total_items) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpSmem<T>& W = reinterpret_cast<WarpSmem<T>*>(smem_raw)[warp];
@@ -375,6 +380,8 @@ __global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const
 template <int G, bool DENSE>
 __global__ void __launch_bounds__(256) merge_kernel(tw_paged_kv kv, tw_decode_buffers buf, float* __restrict__ out,
                                                     int chunk, int max_chunks) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float w[2048];
   __shared__ float Lsum[8];
   __shared__ __align__(16) float red[8][G * kHeadDim];
@@ -467,8 +474,8 @@ static int launch_attn(const tw_paged_kv* kv, const T* q, const tw_decode_buffer
   int grid = sms * persist_cap(per_sm);
   if (DENSE && grid * kAttWarps > total) grid = (total + kAttWarps - 1) / kAttWarps;
   if (DENSE) cudaMemsetAsync(buf->counters + 5, 0, sizeof(uint32_t), s);  // dense runs without tw_select
-  kern<<<grid, kAttThreads, smem, s>>>(*kv, q, *buf, out, chunk, max_chunks, total);
-  merge_kernel<G, DENSE><<<units, 256, 0, s>>>(*kv, *buf, out, chunk, max_chunks);
+  launch_pdl(kern, dim3(grid), dim3(kAttThreads), smem, s, *kv, q, *buf, out, chunk, max_chunks, total);
+  launch_pdl(merge_kernel<G, DENSE>, dim3(units), dim3(256), 0, s, *kv, *buf, out, chunk, max_chunks);
   return launch_status();
 }
 

@@ -1,6 +1,7 @@
 // Shared device helpers for the Twilight sm_100a kernels.
 #pragma once
 #include <cstdlib>
+#include <utility>
 
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -187,6 +188,36 @@ __device__ __forceinline__ int warp_fetch(uint32_t* ctr) {
 
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Programmatic dependent launch (PDL): kernels of the decode step are launched
+// with programmatic stream serialization, so a kernel's CTAs can be scheduled
+// while its predecessor drains; each waits (griddepcontrol.wait) before
+// touching the predecessor's outputs.  TW_PDL=0 turns it off (A/B knob).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("TW_PDL");
+    on = e ? atoi(e) != 0 : 0;  // measured no gain inside CUDA graphs (r01): off by default
+  }
+  return on != 0;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // Experiment knob: cap the resident CTAs per SM of the persistent kernels

@@ -125,6 +125,8 @@ __device__ __forceinline__ void estimate_prologue(const T* __restrict__ q, int u
 template <typename T, int G>
 __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv, const T* __restrict__ q,
                                                                   tw_decode_buffers buf, int max_chunks) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ __align__(128) uint8_t ring[kEstWarps][kEstStages][kQBlockBytes];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane & 3, r = lane >> 2;
@@ -282,7 +284,7 @@ static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode
   const int items = kv->num_seqs * kv->num_kv_heads * max_chunks;
   int grid = sms * persist_cap(per_sm);
   if (grid * kEstWarps > items) grid = (items + kEstWarps - 1) / kEstWarps;
-  estimate_kernel<T, G><<<grid, kEstWarps * 32, 0, stream>>>(*kv, q, *buf, max_chunks);
+  launch_pdl(estimate_kernel<T, G>, dim3(grid), dim3(kEstWarps * 32), 0, stream, *kv, q, *buf, max_chunks);
 }
 
 template <typename T>
@@ -301,7 +303,7 @@ extern "C" int tw_estimate(const tw_paged_kv* kv, const void* q, const tw_decode
                            const tw_decode_buffers* buf, cudaStream_t stream) {
   (void)prm;
   if (!kv || !q || !buf || kv->head_dim != kHeadDim || !buf->logits || !buf->head_max) return TW_ERR_INVALID;
-  cudaMemsetAsync(buf->head_max, 0, sizeof(uint32_t) * kv->num_seqs * kv->num_kv_heads * kv->group_size, stream);
+  // head_max is zeroed by tw_select (quest_select_kernel), which always precedes this call
   if (kv->dtype == TW_BF16) return launch_estimate<__nv_bfloat16>(kv, (const __nv_bfloat16*)q, buf, stream);
   return launch_estimate<float>(kv, (const float*)q, buf, stream);
 }

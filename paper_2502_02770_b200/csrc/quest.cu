@@ -167,6 +167,8 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
                                                                          const __nv_bfloat16* __restrict__ q,
                                                                          float* __restrict__ scores, int max_chunks,
                                                                          uint32_t* __restrict__ ctr) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) uint8_t qm_ring[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane & 3, r = lane >> 2, q8 = lane >> 3, rr = lane & 7;
@@ -328,6 +330,8 @@ struct SelGroupSmem {
 template <typename T>
 __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv kv, const T* __restrict__ q,
                                                                    tw_decode_params prm, tw_decode_buffers buf) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SelGroupSmem GS[kSelGroups];
   __shared__ uint32_t btmp[kSelThreads / 32];
@@ -351,6 +355,7 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
   SelGroupSmem& gs = GS[gp];
 
   STRACE();
+  if ((int)threadIdx.x < G) buf.head_max[(size_t)unit * G + threadIdx.x] = 0u;  // estimate's running max starts at 0
   for (int i = threadIdx.x; i < words; i += blockDim.x) ubits[i] = 0;
   const int k = min(P, prm.budget_pages);
   const int* pt = kv.page_table + (size_t)b * Pmax;
@@ -495,8 +500,8 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQfWarps * 32, smem);
         int grid = sms * persist_cap(per_sm);
         if (grid * kQfWarps > items) grid = (items + kQfWarps - 1) / kQfWarps;
-        kern<<<grid, kQfWarps * 32, smem, stream>>>(*kv, (const __nv_bfloat16*)q, buf->page_scores, max_chunks,
-                                                   buf->counters + 2);
+        launch_pdl(kern, dim3(grid), dim3(kQfWarps * 32), smem, stream, *kv, (const __nv_bfloat16*)q,
+                   buf->page_scores, max_chunks, buf->counters + 2);
       };
       switch (kv->group_size) {
         case 1: gom(quest_filter_mma_kernel<1>); break;
@@ -518,13 +523,14 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
   const size_t smem = select_smem_bytes(kv->max_pages);
   if (smem > 227 * 1024) return TW_ERR_INVALID;
   cudaFuncSetAttribute(quest_select_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  quest_select_kernel<T><<<units, kSelThreads, smem, stream>>>(*kv, (const T*)q, *prm, *buf);
+  launch_pdl(quest_select_kernel<T>, dim3(units), dim3(kSelThreads), smem, stream, *kv, (const T*)q, *prm, *buf);
   return launch_status();
 }
 
 extern "C" int tw_select(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
                          const tw_decode_buffers* buf, cudaStream_t stream) {
-  if (!kv || !prm || !buf || kv->head_dim != kHeadDim || !buf->cand_pages || !buf->cand_count || !buf->counters)
+  if (!kv || !prm || !buf || kv->head_dim != kHeadDim || !buf->cand_pages || !buf->cand_count || !buf->counters ||
+      !buf->head_max)
     return TW_ERR_INVALID;
   if (prm->selector != TW_SELECT_FULL && prm->selector != TW_SELECT_QUEST) return TW_ERR_INVALID;
   if (prm->selector == TW_SELECT_QUEST &&

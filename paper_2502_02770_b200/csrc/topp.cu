@@ -37,6 +37,20 @@
 
 namespace tw {
 
+#ifdef TW_TOPP_TRACE
+__device__ unsigned long long g_tt[1024][8];
+#define TT(ph)                                                                                       \
+  do {                                                                                               \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {                                                     \
+      unsigned long long now_;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));                                      \
+      g_tt[blockIdx.x][ph] = now_;                                                                   \
+    }                                                                                                \
+  } while (0)
+#else
+#define TT(ph) do {} while (0)
+#endif
+
 constexpr int kBins = TW_TOPP_BINS;      // 4096
 constexpr float kBinPerLogit = 120.0f;   // bins cover (max - z) in [0, 34.1); the last bin takes the rest
 constexpr int kHB = 4;                   // heads whose histograms are resident at once (4 x 32 KB)
@@ -46,11 +60,10 @@ constexpr int kRankCap = 64;             // members ranked exactly (O(k^2))
 constexpr float kUscale = 4194304.0f;    // deficits in units of 2^-22
 constexpr double kInvUscale = 1.0 / 4194304.0;
 // exp(-i/120), i = 0..15
-__constant__ double kStepExp[16] = {
-    1.0, 0.991701292638876, 0.9834714538216175, 0.9753099120283326, 0.9672161004820059, 0.9591894571091382,
-    0.951229424500714, 0.9433354498734922, 0.9355069850316178, 0.9277434863285529, 0.9200444146293233,
-    0.9124092352730778, 0.9048374180359595, 0.8973284370942841, 0.8898817709880238, 0.8824969025845955};
-
+__constant__ float kStepExpF[16] = {
+    1.0f, 0.991701292638876f, 0.9834714538216175f, 0.9753099120283326f, 0.9672161004820059f, 0.9591894571091382f,
+    0.951229424500714f, 0.9433354498734922f, 0.9355069850316178f, 0.9277434863285529f, 0.9200444146293233f,
+    0.9124092352730778f, 0.9048374180359595f, 0.8973284370942841f, 0.8898817709880238f, 0.8824969025845955f};
 // Masses.  Bin b of (max - z) has top t_b = M - b/120 (float) and weight
 // w_b = exp(t_b - M) (fp64).  A member has e_i = exp(z_i - M) = w_b r_i with
 // r_i = exp(z_i - t_b) in (0.9917, 1]; it is summed as the fixed-point deficit
@@ -273,31 +286,37 @@ struct HeadRec {
   int seg;            // member-list segment start (-1: resolved by re-reading the logits)
 };
 
-template <int G>
+// HB = heads whose histograms are resident at once.  The wide variant (HB = 4)
+// runs one 1024-thread CTA per SM; the narrow one (HB = 2 for G = 4, half the
+// member list) fits two per SM, for batches with more units than SMs.
+template <int G, int HB>
 struct UnitCfg {
-  static constexpr int GB = G < kHB ? G : kHB;  // heads per histogram batch
+  static constexpr int GB = G < HB ? G : HB;    // heads per histogram batch
   static constexpr int GT = G <= 2 ? 512 : 256;  // threads per head (warp group)
   static constexpr int NT = GT * GB;            // threads
+  static constexpr int MC = HB >= kHB ? kMemberCap : kMemberCap / 2;  // member-list capacity
   static constexpr size_t kHistBytes = (size_t)GB * kBins * 8;
   static constexpr size_t kResBytes = (size_t)GB * sizeof(ResGroupSmem);
-  static constexpr size_t kSmem = (kHistBytes > kResBytes ? kHistBytes : kResBytes) + (size_t)kMemberCap * 8;
+  static constexpr size_t kSmem = (kHistBytes > kResBytes ? kHistBytes : kResBytes) + (size_t)MC * 8;
 };
 
-template <int G>
-__global__ void __launch_bounds__(UnitCfg<G>::NT) topp_unit_kernel(tw_paged_kv kv, tw_decode_params prm,
-                                                                  tw_decode_buffers buf) {
-  constexpr int GB = UnitCfg<G>::GB, NT = UnitCfg<G>::NT, kGT = UnitCfg<G>::GT;
+template <int G, int HB>
+__global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_kv kv, tw_decode_params prm,
+                                                                      tw_decode_buffers buf) {
+  pdl_wait();
+  pdl_trigger();
+  using Cfg = UnitCfg<G, HB>;
+  constexpr int GB = Cfg::GB, NT = Cfg::NT, kGT = Cfg::GT, MC = Cfg::MC;
   constexpr int kPerT = kBins / kGT;  // bins per thread in the crossing scan
   extern __shared__ __align__(16) unsigned char sm[];
   uint32_t* Hc = reinterpret_cast<uint32_t*>(sm);                           // [GB][kBins] counts
   uint32_t* Hu = Hc + GB * kBins;                                            // [GB][kBins] deficit sums
   ResGroupSmem* RS = reinterpret_cast<ResGroupSmem*>(sm);                    // [GB] (aliases the bins)
-  uint32_t* mkey = reinterpret_cast<uint32_t*>(sm + UnitCfg<G>::kSmem - (size_t)kMemberCap * 8);  // [cap]
-  uint32_t* mpos = mkey + kMemberCap;                                        // [cap]
+  uint32_t* mkey = reinterpret_cast<uint32_t*>(sm + Cfg::kSmem - (size_t)MC * 8);  // [MC]
+  uint32_t* mpos = mkey + MC;                                                 // [MC]
   __shared__ HeadRec R[G];
   __shared__ unsigned long long s_deep[GB];
   __shared__ int s_fill[G];
-  __shared__ uint32_t btmp[NT / 32];
   __shared__ int s_first;
   const int unit = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gp = tid / kGT;
@@ -319,6 +338,7 @@ __global__ void __launch_bounds__(UnitCfg<G>::NT) topp_unit_kernel(tw_paged_kv k
     s_fill[tid] = 0;
   }
   __syncthreads();
+  TT(0);
 
   // ---- pass 1 (per batch of GB heads): bins, then each head's crossing bin
 #pragma unroll 1
@@ -365,6 +385,7 @@ __global__ void __launch_bounds__(UnitCfg<G>::NT) topp_unit_kernel(tw_paged_kv k
       }
     }
     __syncthreads();
+    TT(1);
     const int g = g0 + gp;
     if (g < G && R[g].cb != -2) {  // uniform per warp group
       const uint32_t* hc = Hc + gp * kBins;
@@ -373,15 +394,19 @@ __global__ void __launch_bounds__(UnitCfg<G>::NT) topp_unit_kernel(tw_paged_kv k
       const float M120 = M * kBinPerLogit;
       const int bfirst = grp.tid * kPerT;
       const float t0 = bin_top(M, bfirst);
-      const double w0 = exp((double)t0 - (double)M);
+      // Bin masses in fp32 (relative error ~2e-7 each, all terms positive, summed in
+      // fp64): the crossing search tolerates that (the top-p contract allows 1e-6),
+      // and fp64 per bin was the slowest part of this phase.
+      const float w0 = (float)exp((double)t0 - (double)M);
       auto mass = [&](int i, uint32_t& c) -> double {
         const int bb = bfirst + i;
         c = hc[bb];
         if (!c) return 0.0;
         const uint64_t us = bb == kBins - 1 ? (uint64_t)s_deep[gp] : (uint64_t)hu[bb];
         // exp(t_b - M) = w0 * exp(t_b - t0);  t_b - t0 = -i/120 + d (d ~ float rounding, tiny)
-        const double d = ((double)bin_top(M, bb) - (double)t0) + (double)i * (1.0 / 120.0);
-        return class_mass(w0 * kStepExp[i] * (1.0 + d * (1.0 + 0.5 * d)), c, us);
+        const float d = (bin_top(M, bb) - t0) + (float)i * (1.0f / 120.0f);
+        const float w = w0 * kStepExpF[i] * (1.0f + d);
+        return (double)(w * ((float)c - (float)us * (float)kInvUscale));
       };
       static_assert(kPerT <= 16, "kStepExp covers 16 bins per thread");
       double local = 0.0;
@@ -399,6 +424,7 @@ __global__ void __launch_bounds__(UnitCfg<G>::NT) topp_unit_kernel(tw_paged_kv k
       __shared__ int s_bin[GB];
       __shared__ double s_above[GB];
       __shared__ uint32_t s_acnt[GB];
+      if (gp == 0) TT(6);
       const double incl = grp_scan<double>(grp, local, s_dtmp[gp], Z);
       const uint32_t cincl = grp_scan<uint32_t>(grp, lc, s_utmp[gp], b0);
       const double target = p_eff * Z;
@@ -423,6 +449,7 @@ __global__ void __launch_bounds__(UnitCfg<G>::NT) topp_unit_kernel(tw_paged_kv k
         }
       }
       grp.sync();
+      if (gp == 0) TT(7);
       if (grp.tid == 0) {
         HeadRec& r = R[g];
         const int cb = s_bin[gp];  // -1: rounding left the target above the total -> keep everything
@@ -444,12 +471,13 @@ __global__ void __launch_bounds__(UnitCfg<G>::NT) topp_unit_kernel(tw_paged_kv k
     }
     __syncthreads();
   }
+  TT(2);
   // member-list segments: heads in order while they fit; the rest re-read their logits
   if (tid == 0) {
     uint32_t acc = 0;
     for (int g = 0; g < G; ++g) {
       HeadRec& r = R[g];
-      if (r.cb >= 0 && acc + r.members <= (uint32_t)kMemberCap) {
+      if (r.cb >= 0 && acc + r.members <= (uint32_t)MC) {
         r.seg = (int)acc;
         acc += r.members;
       } else if (r.cb >= 0) {
@@ -493,6 +521,7 @@ __global__ void __launch_bounds__(UnitCfg<G>::NT) topp_unit_kernel(tw_paged_kv k
   }
   __syncthreads();
 
+  TT(3);
   // ---- resolve: exact threshold class inside each head's crossing bin (warp group per head)
 #pragma unroll 1
   for (int g = gp; g < G; g += GB) {
@@ -545,32 +574,42 @@ __global__ void __launch_bounds__(UnitCfg<G>::NT) topp_unit_kernel(tw_paged_kv k
     grp.sync();
   }
   __syncthreads();  // member bits (global atomics of this CTA) are visible to its ld.cg below
+  TT(4);
 
-  // ---- K3c: compact the union bitmap -> ascending token ids + attention work items
+  // ---- K3c: compact the union bitmap -> ascending token ids + attention work items.
+  // Each warp owns a contiguous run of words: one pass counts, one CTA scan of
+  // the warp totals, then each warp emits its run (lane l writes bit l of a
+  // word: consecutive lanes -> consecutive ids, coalesced) with no further barriers.
   const int* cand = buf.cand_pages + (size_t)unit * kv.max_pages;
   int* out = buf.final_idx + (size_t)unit * T;
   const int words = (npos + 31) >> 5;
-  uint32_t basei = 0;
-  // the warp owns words w0 + 32 warp + j (j = lane) and their 64 candidate pages;
-  // the next block's words and pages are prefetched while this one is written
-  auto fetch = [&](int w0, uint32_t& x, int& pa, int& pb) {
-    const int w = w0 + tid;
-    x = w < words ? __ldcg(ubits + w) : 0u;
-    const int p0 = 2 * (w0 + 32 * warp);
-    pa = p0 + lane < kv.max_pages ? cand[p0 + lane] : 0;
-    pb = p0 + 32 + lane < kv.max_pages ? cand[p0 + 32 + lane] : 0;
-  };
-  uint32_t xn;
-  int pan, pbn;
-  fetch(0, xn, pan, pbn);
-  for (int w0 = 0; w0 < words; w0 += NT) {
-    const uint32_t x = xn;
-    const int pa = pan, pb = pbn;
-    if (w0 + NT < words) fetch(w0 + NT, xn, pan, pbn);
-    uint32_t total;
-    const uint32_t incl = block_incl_scan(__popc(x), btmp, total);
-    const uint32_t wbase = basei + incl - __popc(x);
-    // lane l writes bit l of each word: consecutive lanes -> consecutive ids (coalesced)
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t s_wtot[NW];
+  const int per_w = (words + NW - 1) / NW;
+  const int wlo = min(words, warp * per_w), whi = min(words, wlo + per_w);
+  uint32_t cnt = 0;
+  for (int w = wlo + lane; w < whi; w += 32) cnt += __popc(__ldcg(ubits + w));
+  cnt = warp_sum(cnt);
+  if (lane == 0) s_wtot[warp] = cnt;
+  __syncthreads();
+  uint32_t run = 0, basei = 0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    run += i < warp ? s_wtot[i] : 0u;
+    basei += s_wtot[i];
+  }
+  for (int w0 = wlo; w0 < whi; w0 += 32) {
+    const int w = w0 + lane;
+    const uint32_t x = w < whi ? __ldcg(ubits + w) : 0u;
+    const int pa = 2 * w0 + lane < kv.max_pages ? cand[2 * w0 + lane] : 0;
+    const int pb = 2 * w0 + 32 + lane < kv.max_pages ? cand[2 * w0 + 32 + lane] : 0;
+    uint32_t incl = __popc(x);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t wbase = run + incl - __popc(x);
 #pragma unroll 4
     for (int j = 0; j < 32; ++j) {
       const uint32_t xw = __shfl_sync(0xffffffffu, x, j);
@@ -580,8 +619,9 @@ __global__ void __launch_bounds__(UnitCfg<G>::NT) topp_unit_kernel(tw_paged_kv k
       if ((xw >> lane) & 1u)
         out[bw + __popc(xw & ((1u << lane) - 1u))] = (j < 16 ? qa : qb) * kPage + (lane & 15);
     }
-    basei += total;
+    run += __shfl_sync(0xffffffffu, incl, 31);
   }
+  TT(5);
   const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : TW_DEFAULT_CHUNK;
   const int nitems = ((int)basei + chunk - 1) / chunk;
   if (tid == 0) {
@@ -668,15 +708,37 @@ __global__ void __launch_bounds__(256) topp_bisect_kernel(const double* __restri
 
 using namespace tw;
 
+#ifdef TW_TOPP_TRACE
+extern "C" int tw_debug_ttrace(unsigned long long* host_out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host_out, g_tt, sizeof(g_tt));
+  static unsigned long long zeros[1024 * 8];
+  cudaMemcpyToSymbol(g_tt, zeros, sizeof(zeros));
+  return 0;
+}
+#endif
+
+template <int G, int HB>
+static int launch_unit_hb(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,
+                          cudaStream_t stream) {
+  const size_t smem = UnitCfg<G, HB>::kSmem;
+  if (cudaFuncSetAttribute(topp_unit_kernel<G, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return TW_ERR_CUDA;
+  launch_pdl(topp_unit_kernel<G, HB>, dim3(kv->num_seqs * kv->num_kv_heads), dim3(UnitCfg<G, HB>::NT), smem, stream,
+             *kv, *prm, *buf);
+  return launch_status();
+}
+
 template <int G>
 static int launch_unit(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,
                        cudaStream_t stream) {
-  const size_t smem = UnitCfg<G>::kSmem;
-  if (cudaFuncSetAttribute(topp_unit_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return TW_ERR_CUDA;
-  topp_unit_kernel<G><<<kv->num_seqs * kv->num_kv_heads, UnitCfg<G>::NT, smem, stream>>>(*kv, *prm, *buf);
-  return launch_status();
+  // more units than SMs: the narrow CTA (two per SM) avoids a second wave of wide CTAs
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (G >= 2 && kv->num_seqs * kv->num_kv_heads > sms) return launch_unit_hb<G, kHB / 2>(kv, prm, buf, stream);
+  return launch_unit_hb<G, kHB>(kv, prm, buf, stream);
 }
 
 extern "C" int tw_topp(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,

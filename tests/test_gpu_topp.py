@@ -144,3 +144,13 @@ def test_topp_p_edges(p):
     check(dec, z, npages, p)
     if p == 0.0:
         assert int(dec.bufs.final_count.sum()) == 0
+
+
+def test_topp_more_units_than_sms():
+    # > 148 units selects the two-CTAs-per-SM variant (half the member list)
+    rng = np.random.default_rng(11)
+    U, G, T = 160, 4, 4096
+    z = _normal(rng, U, G, T, (2.0, 0.5, 1.0, 0.25))
+    npages = [int(x) for x in rng.integers(1, T // 16 + 1, size=U)]
+    dec = run_topp(z, npages, 0.9)
+    check(dec, z, npages, 0.9)
