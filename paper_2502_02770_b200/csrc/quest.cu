@@ -362,8 +362,8 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
   const T* meta = reinterpret_cast<const T*>(kv.kmeta);
   __syncthreads();
 
-  if (prm.selector == TW_SELECT_FULL || k >= P) {
-    for (int i = threadIdx.x; i < P; i += blockDim.x) atomicOr(&ubits[i >> 5], 1u << (i & 31));
+  const bool all = prm.selector == TW_SELECT_FULL || k >= P;
+  if (all) {
     if (buf.head_page_bits) {
       for (int g = 0; g < G; ++g)
         for (int i = threadIdx.x; i < words; i += blockDim.x) {
@@ -443,6 +443,11 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
   STRACE();
   // compact the union bitmap -> ascending candidate page list
   int* out = buf.cand_pages + (size_t)unit * Pmax;
+  if (all) {  // every page: no bitmap
+    for (int i = threadIdx.x; i < P; i += blockDim.x) out[i] = i;
+    if (threadIdx.x == 0) buf.cand_count[unit] = P;
+    return;
+  }
   uint32_t base = 0;
   for (int w0 = 0; w0 < words; w0 += blockDim.x) {
     const int w = w0 + threadIdx.x;

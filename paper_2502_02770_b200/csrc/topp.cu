@@ -398,6 +398,9 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
       // fp64): the crossing search tolerates that (the top-p contract allows 1e-6),
       // and fp64 per bin was the slowest part of this phase.
       const float w0 = (float)exp((double)t0 - (double)M);
+#ifdef TW_TT_SPLIT
+      if (gp == 0) TT(6);
+#endif
       auto mass = [&](int i, uint32_t& c) -> double {
         const int bb = bfirst + i;
         c = hc[bb];
@@ -424,7 +427,9 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
       __shared__ int s_bin[GB];
       __shared__ double s_above[GB];
       __shared__ uint32_t s_acnt[GB];
+#ifndef TW_TT_SPLIT
       if (gp == 0) TT(6);
+#endif
       const double incl = grp_scan<double>(grp, local, s_dtmp[gp], Z);
       const uint32_t cincl = grp_scan<uint32_t>(grp, lc, s_utmp[gp], b0);
       const double target = p_eff * Z;
