@@ -52,7 +52,7 @@ typedef enum {
 } tw_status;
 
 typedef enum { TW_F32 = 0, TW_BF16 = 1 } tw_dtype;
-typedef enum { TW_SELECT_FULL = 0, TW_SELECT_QUEST = 1 } tw_selector;
+typedef enum { TW_SELECT_FULL = 0, TW_SELECT_QUEST = 1, TW_SELECT_SINK_WINDOW = 2 } tw_selector;
 
 typedef struct tw_paged_kv {
   int32_t num_seqs;       /* B */
@@ -73,11 +73,13 @@ typedef struct tw_paged_kv {
 } tw_paged_kv;
 
 typedef struct tw_decode_params {
-  int32_t selector;     /* tw_selector: full (selectors.py:90-94) or quest (:112-132) */
+  int32_t selector;     /* tw_selector: full (selectors.py:90-94), quest (:112-132), sink_window (:164-175) */
   int32_t budget_pages; /* ceil(B0 / 16), B0 = resolve_budget(...) (selectors.py:72-87, :127) */
   double p;             /* top-p mass target, BinarySearchConfig.p (pruner.py:35) */
   int32_t chunk_tokens; /* sparse-attention work-item size (0 = TW_DEFAULT_CHUNK) */
   int32_t renormalize;  /* must be 1 on this path (PipelineConfig.renormalize_output, pipeline.py:58) */
+  int32_t sink;         /* sink-window selector (select_sink_window, selectors.py:164-175): first tokens kept */
+  int32_t window;       /* ... and last tokens kept; every token when sink + window >= n */
 } tw_decode_params;
 
 /* Intermediate buffers of one decode step (all caller-allocated, sizes in

@@ -185,14 +185,22 @@ def main() -> None:
         ("head_full_bf16", 600, 1, "full", None, 0.9, 0.4, "bf16"),
         ("head_quest_f32", 777, 1, "quest", 200, 0.8, 1.0, "f32"),
         ("grouped_full_f32", 640, 2, "full", None, 0.99, 2.0, "f32"),
+        # sink-window base selector (selectors.py:164-175): sink/window in tokens
+        ("grouped_sinkwin_bf16", 900, 4, "sink_window:7:150", None, 0.9, 0.3, "bf16"),
+        ("head_sinkwin_f32", 500, 1, "sink_window:0:33", None, 0.95, 0.5, "f32"),
+        ("grouped_sinkwin_all_f32", 300, 2, "sink_window:200:120", None, 0.9, 1.0, "f32"),
     ]
     for name, n, G, kind, budget, p, tau, dt in configs:
+        sink = window = 0
+        if kind.startswith("sink_window"):
+            kind, sink, window = kind.split(":")[0], int(kind.split(":")[1]), int(kind.split(":")[2])
         K = rng.standard_normal((n, 128)).astype(np.float32)
         V = rng.standard_normal((n, 128)).astype(np.float32)
         Q = (rng.standard_normal((G, 128)) / tau).astype(np.float32)
         if dt == "bf16":
             K, V, Q = bf16_round(K), bf16_round(V), bf16_round(Q)
-        sel = nk.SelectorConfig(kind=kind, budget=budget, page_size=16)
+        sel = nk.SelectorConfig(kind=kind, budget=budget, page_size=16, **(
+            dict(sink=sink, window=window) if kind == "sink_window" else {}))
         cfg = nk.PipelineConfig(selector=sel, prune=nk.BinarySearchConfig(p=p), group_map=nk.GroupMap(G))
         if G == 1:
             out, outcome, report = nk.run_head(Q[0], K, V, cfg)
@@ -201,8 +209,10 @@ def main() -> None:
             outs, outcomes, reports = nk.run_grouped(Q, K, V, cfg)
             finals, b0 = [o.selection.indices for o in outcomes], [r.b0 for r in reports]
         pipe[f"{name}/K"], pipe[f"{name}/V"], pipe[f"{name}/Q"] = K, V, Q
-        pipe[f"{name}/cfg"] = np.array([-1 if budget is None else budget, p, 1.0 if kind == "quest" else 0.0,
-                                        1.0 if isinstance(budget, float) else 0.0])
+        # budget, p, selector (0 full, 1 quest, 2 sink_window), budget-is-fraction, sink, window
+        pipe[f"{name}/cfg"] = np.array([-1 if budget is None else budget, p,
+                                        {"full": 0.0, "quest": 1.0, "sink_window": 2.0}[kind],
+                                        1.0 if isinstance(budget, float) else 0.0, sink, window])
         pipe[f"{name}/out"] = np.asarray(outs)
         pipe[f"{name}/final"] = finals[0]
         pipe[f"{name}/b0"] = np.array(b0)

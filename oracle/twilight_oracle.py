@@ -183,6 +183,20 @@ def pages_to_tokens(pages: np.ndarray, n: int, page_size: int = PAGE_SIZE) -> np
     return tok[tok < n]
 
 
+def sink_window_tokens(n: int, sink: int, window: int) -> np.ndarray:
+    """select_sink_window (selectors.py:164-175): the first ``sink`` plus the
+    last ``window`` tokens; every token when they meet (select_full)."""
+    if n < 1:
+        raise ValueError("context must contain at least one token")
+    if sink < 0 or window < 0:
+        raise ValueError("sink and window must be non-negative")
+    if sink + window < 1:
+        raise ValueError("sink + window must keep at least one token")
+    if sink + window >= n:
+        return np.arange(n, dtype=np.int64)
+    return np.unique(np.concatenate([np.arange(sink), np.arange(n - window, n)])).astype(np.int64)
+
+
 def union_sorted(index_sets) -> np.ndarray:
     """Sorted union of index arrays (group_union, selectors.py:178-186)."""
     sets = [np.asarray(s, dtype=np.int64) for s in index_sets]
@@ -346,15 +360,19 @@ def prepare_unit(K, page_size: int = PAGE_SIZE):
 
 
 def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.95,
-                page_size: int = PAGE_SIZE, renormalize: bool = True, logits_override=None, prepared=None):
+                page_size: int = PAGE_SIZE, renormalize: bool = True, logits_override=None, prepared=None,
+                sink: int = 4, window: int = 64):
     """run_grouped's hot path for one KV head (pipeline.py:306-360):
 
-    per-head Quest (selectors.py:112-132) -> group union (:338) -> per-head
+    per-head Quest (selectors.py:112-132; or select_full :90-94, or
+    select_sink_window :164-175, whose token set is the candidates directly) ->
+    group union (:338) -> per-head
     INT4 estimate over the union (:342) -> fp64 softmax (:344) -> threshold
     search (:345) -> group set = union of the pruned sets (:347) -> every
     head attends to the group set with renormalised full-context weights
     (:366-375).  With G == 1 this is run_head (pipeline.py:286-303; equal
-    per test_pipeline.py:232-241).  ``selector`` is "quest" or "full".
+    per test_pipeline.py:232-241).  ``selector`` is "quest", "full" or
+    "sink_window".
 
     ``logits_override`` (G, |union|) replaces the INT4 estimate, so a test
     can feed the GPU's logits to the oracle's softmax + search;
@@ -369,10 +387,16 @@ def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.9
         head_pages = [np.arange(lo.shape[0]) for _ in range(G)]
     elif selector == "quest":
         head_pages = [quest_select_pages(Q[h], lo, hi, budget, n, page_size) for h in range(G)]
+    elif selector == "sink_window":
+        head_pages = None
     else:
         raise ValueError(f"selector {selector!r} not on the accelerated path")
-    union_pages = union_sorted(head_pages)
-    cand = pages_to_tokens(union_pages, n, page_size)
+    if head_pages is None:
+        cand = sink_window_tokens(n, sink, window)  # the same for every head: the union is the set itself
+        union_pages = np.unique(cand // page_size)
+    else:
+        union_pages = union_sorted(head_pages)
+        cand = pages_to_tokens(union_pages, n, page_size)
     logits, pruned, thresholds, iters = [], [], [], []
     for h in range(G):
         z = estimate_logits(Q[h], codes, scale, zero, cand) if logits_override is None \

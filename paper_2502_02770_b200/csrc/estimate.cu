@@ -124,7 +124,8 @@ __device__ __forceinline__ void estimate_prologue(const T* __restrict__ q, int u
 // each warp streams its pages' 1152-B INT4 blocks through a 4-deep cp.async ring.
 template <typename T, int G>
 __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv, const T* __restrict__ q,
-                                                                  tw_decode_buffers buf, int max_chunks) {
+                                                                  tw_decode_buffers buf, int max_chunks,
+                                                                  int sw_sink, int sw_window) {
   pdl_wait();
   pdl_trigger();
   __shared__ __align__(128) uint8_t ring[kEstWarps][kEstStages][kQBlockBytes];
@@ -215,7 +216,10 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       for (int e = 0; e < 4; ++e)
         d[e] = fmaf((float)acc[2][e], 65536.f, fmaf((float)acc[1][e], 256.f, (float)acc[0][e])) * isc[e & 1];
       const int tok_r = lp * kPage + r;
-      const bool v_r = tok_r < n, v_r8 = tok_r + 8 < n;
+      // sink-window selection (selectors.py:164-175): tokens between the sink and the window are not candidates
+      const bool swm = sw_window >= 0 && sw_sink + sw_window < n;
+      const bool v_r = tok_r < n && (!swm || tok_r < sw_sink || tok_r >= n - sw_window);
+      const bool v_r8 = tok_r + 8 < n && (!swm || tok_r + 8 < sw_sink || tok_r + 8 >= n - sw_window);
       const int ci = c0 + i;
       if (2 * t < G) {
 #pragma unroll
@@ -275,7 +279,8 @@ __global__ void estimate_tokens_kernel(tw_paged_kv kv, int seq, int kvh, const T
 using namespace tw;
 
 template <typename T, int G>
-static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, cudaStream_t stream) {
+static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, int sw_sink,
+                              int sw_window, cudaStream_t stream) {
   const int max_chunks = (kv->max_pages + kEstPagesPerCta - 1) / kEstPagesPerCta;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
@@ -284,16 +289,18 @@ static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode
   const int items = kv->num_seqs * kv->num_kv_heads * max_chunks;
   int grid = sms * persist_cap(per_sm);
   if (grid * kEstWarps > items) grid = (items + kEstWarps - 1) / kEstWarps;
-  launch_pdl(estimate_kernel<T, G>, dim3(grid), dim3(kEstWarps * 32), 0, stream, *kv, q, *buf, max_chunks);
+  launch_pdl(estimate_kernel<T, G>, dim3(grid), dim3(kEstWarps * 32), 0, stream, *kv, q, *buf, max_chunks, sw_sink,
+             sw_window);
 }
 
 template <typename T>
-static int launch_estimate(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, cudaStream_t stream) {
+static int launch_estimate(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, int ss, int sw,
+                           cudaStream_t stream) {
   switch (kv->group_size) {
-    case 1: launch_estimate_g<T, 1>(kv, q, buf, stream); break;
-    case 2: launch_estimate_g<T, 2>(kv, q, buf, stream); break;
-    case 4: launch_estimate_g<T, 4>(kv, q, buf, stream); break;
-    case 8: launch_estimate_g<T, 8>(kv, q, buf, stream); break;
+    case 1: launch_estimate_g<T, 1>(kv, q, buf, ss, sw, stream); break;
+    case 2: launch_estimate_g<T, 2>(kv, q, buf, ss, sw, stream); break;
+    case 4: launch_estimate_g<T, 4>(kv, q, buf, ss, sw, stream); break;
+    case 8: launch_estimate_g<T, 8>(kv, q, buf, ss, sw, stream); break;
     default: return TW_ERR_INVALID;
   }
   return launch_status();
@@ -301,11 +308,12 @@ static int launch_estimate(const tw_paged_kv* kv, const T* q, const tw_decode_bu
 
 extern "C" int tw_estimate(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
                            const tw_decode_buffers* buf, cudaStream_t stream) {
-  (void)prm;
   if (!kv || !q || !buf || kv->head_dim != kHeadDim || !buf->logits || !buf->head_max) return TW_ERR_INVALID;
+  const bool sw = prm && prm->selector == TW_SELECT_SINK_WINDOW;
+  const int ss = sw ? prm->sink : 0, swin = sw ? prm->window : -1;
   // head_max is zeroed by tw_select (quest_select_kernel), which always precedes this call
-  if (kv->dtype == TW_BF16) return launch_estimate<__nv_bfloat16>(kv, (const __nv_bfloat16*)q, buf, stream);
-  return launch_estimate<float>(kv, (const float*)q, buf, stream);
+  if (kv->dtype == TW_BF16) return launch_estimate<__nv_bfloat16>(kv, (const __nv_bfloat16*)q, buf, ss, swin, stream);
+  return launch_estimate<float>(kv, (const float*)q, buf, ss, swin, stream);
 }
 
 extern "C" int tw_estimate_tokens(const tw_paged_kv* kv, int32_t seq, int32_t kv_head, const void* q,

@@ -362,8 +362,24 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
   const T* meta = reinterpret_cast<const T*>(kv.kmeta);
   __syncthreads();
 
-  const bool all = prm.selector == TW_SELECT_FULL || k >= P;
-  if (all) {
+  // sink-window (selectors.py:164-175): pages [0, sw_a) and [sw_b, P); every page when the two meet
+  const bool sw = prm.selector == TW_SELECT_SINK_WINDOW;
+  const int sw_a = sw ? (prm.sink + kPage - 1) / kPage : 0;
+  const int sw_b = sw ? max(0, n - prm.window) / kPage : 0;
+  const bool all = prm.selector == TW_SELECT_FULL || (!sw && k >= P) ||
+                   (sw && (prm.sink + prm.window >= n || sw_b <= sw_a));
+  if (sw && !all) {
+    if (buf.head_page_bits)
+      for (int g = 0; g < G; ++g)
+        for (int i = threadIdx.x; i < words; i += blockDim.x) {
+          uint32_t w = 0;
+          for (int j = 0; j < 32; ++j) {
+            const int pg = i * 32 + j;
+            w |= (pg < P && (pg < sw_a || pg >= sw_b)) ? 1u << j : 0u;
+          }
+          buf.head_page_bits[((size_t)unit * G + g) * words + i] = w;
+        }
+  } else if (all) {
     if (buf.head_page_bits) {
       for (int g = 0; g < G; ++g)
         for (int i = threadIdx.x; i < words; i += blockDim.x) {
@@ -446,6 +462,12 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
   if (all) {  // every page: no bitmap
     for (int i = threadIdx.x; i < P; i += blockDim.x) out[i] = i;
     if (threadIdx.x == 0) buf.cand_count[unit] = P;
+    return;
+  }
+  if (sw) {  // two page ranges
+    const int nb = P - sw_b;
+    for (int i = threadIdx.x; i < sw_a + nb; i += blockDim.x) out[i] = i < sw_a ? i : sw_b + (i - sw_a);
+    if (threadIdx.x == 0) buf.cand_count[unit] = sw_a + nb;
     return;
   }
   uint32_t base = 0;
@@ -537,7 +559,10 @@ extern "C" int tw_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
   if (!kv || !prm || !buf || kv->head_dim != kHeadDim || !buf->cand_pages || !buf->cand_count || !buf->counters ||
       !buf->head_max)
     return TW_ERR_INVALID;
-  if (prm->selector != TW_SELECT_FULL && prm->selector != TW_SELECT_QUEST) return TW_ERR_INVALID;
+  if (prm->selector != TW_SELECT_FULL && prm->selector != TW_SELECT_QUEST && prm->selector != TW_SELECT_SINK_WINDOW)
+    return TW_ERR_INVALID;
+  if (prm->selector == TW_SELECT_SINK_WINDOW && (prm->sink < 0 || prm->window < 0 || prm->sink + prm->window < 1))
+    return TW_ERR_INVALID;
   if (prm->selector == TW_SELECT_QUEST &&
       (prm->budget_pages < 1 || !buf->page_scores || !buf->band_idx || !buf->band_scores || !q))
     return TW_ERR_INVALID;

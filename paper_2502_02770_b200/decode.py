@@ -224,12 +224,13 @@ def budget_pages_for(budget, n: int) -> int:
 class TwilightDecoder:
     """Runs the select -> estimate -> prune -> attend path for one layer.
 
-    selector: "quest" (Quest page top-k with budget B0 tokens) or "full".
+    selector: "quest" (Quest page top-k with budget B0 tokens), "full", or
+    "sink_window" (the first ``sink`` + last ``window`` tokens, selectors.py:164-175).
     """
 
     def __init__(self, cache: PagedKVCache, selector: str = "quest", budget=None, p: float = 0.95,
                  chunk_tokens: int | None = None, head_page_bits: bool = False,
-                 bufs: DecodeBuffers | list | None = None, waves: int = 1):
+                 bufs: DecodeBuffers | list | None = None, waves: int = 1, sink: int = 4, window: int = 64):
         self.waves = []
         if waves > 1:
             # sub-batches on their own streams: the select/top-p stages of one wave
@@ -239,29 +240,34 @@ class TwilightDecoder:
             per = cache.num_seqs // waves
             for w in range(waves):
                 sub = TwilightDecoder(cache.view(w * per, (w + 1) * per), selector, budget, p, chunk_tokens,
-                                      head_page_bits, bufs[w] if isinstance(bufs, list) else None)
+                                      head_page_bits, bufs[w] if isinstance(bufs, list) else None,
+                                      sink=sink, window=window)
                 self.waves.append((w * per, (w + 1) * per, sub, torch.cuda.Stream(device=cache.device)))
             self.cache = cache
             self.params = self.waves[0][2].params
             self.bufs = [wv[2].bufs for wv in self.waves]
             return
         chunk_tokens = chunk_tokens or auto_chunk(cache)
-        if selector not in ("quest", "full"):
-            raise ValueError(f"selector {selector!r} is not on the accelerated path (quest | full)")
+        if selector not in ("quest", "full", "sink_window"):
+            raise ValueError(f"selector {selector!r} is not on the accelerated path (quest | full | sink_window)")
+        if selector == "sink_window" and (sink < 0 or window < 0 or sink + window < 1):
+            raise ValueError("sink and window must be non-negative and keep at least one token")
         if not 0.0 <= p <= 1.0:
             raise ValueError(f"p={p} outside [0, 1]")
         self.cache = cache
         # buffers may be shared by decoders of layers with the same geometry
         self.bufs = bufs if bufs is not None else DecodeBuffers(cache, chunk_tokens, head_page_bits)
         self.params = L.TwDecodeParams()
-        self.params.selector = L.TW_SELECT_QUEST if selector == "quest" else L.TW_SELECT_FULL
+        self.params.selector = {"quest": L.TW_SELECT_QUEST, "full": L.TW_SELECT_FULL,
+                                "sink_window": L.TW_SELECT_SINK_WINDOW}[selector]
+        self.params.sink, self.params.window = int(sink), int(window)
         self.params.p = float(p)
         self.params.chunk_tokens = chunk_tokens
         self.params.renormalize = 1
         self.set_budget(budget)
 
     def set_budget(self, budget, n: int | None = None) -> None:
-        if self.params.selector == L.TW_SELECT_FULL:
+        if self.params.selector in (L.TW_SELECT_FULL, L.TW_SELECT_SINK_WINDOW):
             self.params.budget_pages = self.cache.max_pages
             return
         if budget is None:

@@ -116,7 +116,7 @@ def _spearman(a: torch.Tensor, b: torch.Tensor) -> float:
 
 
 def _check_cfg(cfg: PipelineConfig) -> None:
-    if cfg.selector.kind not in ("full", "quest"):
+    if cfg.selector.kind not in ("full", "quest", "sink_window"):
         raise NotImplementedError(f"selector {cfg.selector.kind!r} is not on the B200 path")
     if cfg.estimator_bits != 4:
         raise NotImplementedError("the B200 path estimates with the 4-bit cache (estimator_bits=4)")
@@ -143,6 +143,8 @@ def _run(Q: torch.Tensor, keys: torch.Tensor, values: torch.Tensor, cfg: Pipelin
         if cfg.selector.budget is None:
             raise ValueError("selector 'quest' requires a budget")
         dec = TwilightDecoder(kv, "quest", budget=resolve_budget(cfg.selector.budget, n), p=cfg.prune.p)
+    elif cfg.selector.kind == "sink_window":
+        dec = TwilightDecoder(kv, "sink_window", p=cfg.prune.p, sink=cfg.selector.sink, window=cfg.selector.window)
     else:
         dec = TwilightDecoder(kv, "full", p=cfg.prune.p)
     q = Q.to(dt).reshape(groups, G, L.HEAD_DIM).contiguous()
@@ -169,8 +171,9 @@ def _reports(dec: TwilightDecoder, Q, keys, values, cfg: PipelineConfig, G: int)
         ncand = int(bufs.cand_count[u].item())
         pages = bufs.cand_pages[u, :ncand].long()
         cand = (pages[:, None] * 16 + torch.arange(16, device=pages.device)).reshape(-1)
-        valid = cand < n
-        logits = bufs.logits[u, g, : ncand * 16][valid]
+        logits = bufs.logits[u, g, : ncand * 16]
+        valid = (cand < n) & torch.isfinite(logits)  # padding and (sink-window) unselected tokens are -inf
+        logits = logits[valid]
         cand = cand[valid]
         est_w = torch.softmax(logits.double(), 0)
         in_final = torch.isin(cand, final)

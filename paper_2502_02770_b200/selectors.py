@@ -1,9 +1,10 @@
 """Candidate selectors with the reference signatures (nucleuskv/selectors.py).
 
 ``quest_page_scores``, ``select_quest`` and ``group_union`` run on the B200
-kernels (tw_quest_scores / tw_select); ``select_full``/``resolve_budget`` are
-host arithmetic.  The channel-pruned and sink-window selectors are not on the
-accelerated path and raise NotImplementedError.
+kernels (tw_quest_scores / tw_select); ``select_full``, ``select_sink_window``
+and ``resolve_budget`` are index arithmetic (the decode path runs sink-window
+selection inside tw_select / tw_estimate).  The channel-pruned selector is not
+on the accelerated path and raises NotImplementedError.
 """
 
 from __future__ import annotations
@@ -130,8 +131,19 @@ def select_channel_pruned(*args, **kwargs):
     raise NotImplementedError("channel-pruned selection is not on the B200 path (SURVEY.md 2.1)")
 
 
-def select_sink_window(*args, **kwargs):
-    raise NotImplementedError("sink-window selection is not on the B200 path (SURVEY.md 2.1)")
+def select_sink_window(n: int, sink: int, window: int, device="cuda") -> TokenSelection:
+    """selectors.py:164-175: the first ``sink`` plus the last ``window`` tokens;
+    every token when they meet."""
+    if n < 1:
+        raise ValueError("context must contain at least one token")
+    if sink < 0 or window < 0:
+        raise ValueError("sink and window must be non-negative")
+    if sink + window < 1:
+        raise ValueError("sink + window must keep at least one token")
+    if sink + window >= n:
+        return select_full(n, device)
+    idx = torch.cat([torch.arange(sink, device=device), torch.arange(n - window, n, device=device)])
+    return TokenSelection.from_indices(idx, n)
 
 
 def top_channels_by_magnitude(*args, **kwargs):
@@ -139,12 +151,14 @@ def top_channels_by_magnitude(*args, **kwargs):
 
 
 def build_selector(cfg: SelectorConfig, keys, metadata=None) -> Callable:
-    """selectors.py:189-209 for the accelerated kinds (full, quest)."""
+    """selectors.py:189-209 for the accelerated kinds (full, quest, sink_window)."""
     n = int(keys.shape[0])
+    dev = keys.device if isinstance(keys, torch.Tensor) else "cuda"
     if cfg.kind == "full":
-        dev = keys.device if isinstance(keys, torch.Tensor) else "cuda"
         return lambda q: select_full(n, dev)
-    if cfg.kind in ("channel_pruned", "sink_window"):
+    if cfg.kind == "sink_window":
+        return lambda q: select_sink_window(n, cfg.sink, cfg.window, dev)
+    if cfg.kind == "channel_pruned":
         raise NotImplementedError(f"selector {cfg.kind!r} is not on the B200 path")
     if cfg.budget is None:
         raise ValueError(f"selector {cfg.kind!r} requires a budget")

@@ -142,16 +142,25 @@ def test_attention_readout_matches_reference(golden):
         tw.sparse_attention(cuda(np.full(4, 0.25)), cuda(np.ones((4, 128))), empty, renormalize=True)
 
 
+def test_select_sink_window_indices():
+    # selectors.py:164-175
+    assert tw.select_sink_window(100, 4, 10).indices.tolist() == list(range(4)) + list(range(90, 100))
+    assert tw.select_sink_window(20, 15, 5).indices.tolist() == list(range(20))  # they meet: every token
+    assert tw.select_sink_window(50, 0, 3).indices.tolist() == [47, 48, 49]
+
+
 def test_run_grouped_and_run_head_match_reference(golden):
     """The whole hot path (K2 -> K3 -> K4 on one context) against run_grouped /
     run_head outputs of the reference: identical final sets up to top-p
     threshold ties, and attention outputs within tolerance."""
     for name, c in golden("pipeline").items():
-        budget, p, is_quest, is_frac = c["cfg"]
+        budget, p, kind, is_frac, sink, window = c["cfg"]
         budget = float(budget) if is_frac else int(budget)
+        selector = ("full", "quest", "sink_window")[int(kind)]
+        is_quest = selector == "quest"
         K, V, Q = as_input(c["K"]), as_input(c["V"]), as_input(c["Q"])
         G = Q.shape[0]
-        sel = tw.SelectorConfig(kind="quest" if is_quest else "full", budget=budget if is_quest else None)
+        sel = tw.SelectorConfig(kind=selector, budget=budget if is_quest else None, sink=int(sink), window=int(window))
         cfg = tw.PipelineConfig(selector=sel, prune=tw.BinarySearchConfig(p=float(p)), group_map=tw.GroupMap(G))
         if G == 1:
             out, outcome, report = tw.run_head(Q[0], K, V, cfg)
@@ -165,7 +174,8 @@ def test_run_grouped_and_run_head_match_reference(golden):
         if not np.array_equal(final, want):
             # allowed only as a top-p tie at the threshold: check each head's set with the oracle
             Kn, Vn, Qn = K.float().cpu().numpy(), V.float().cpu().numpy(), Q.float().cpu().numpy()
-            res = orc.decode_unit(Qn, Kn, Vn, selector="quest" if is_quest else "full", budget=budget, p=float(p))
+            res = orc.decode_unit(Qn, Kn, Vn, selector=selector, budget=budget, p=float(p), sink=int(sink),
+                                  window=int(window))
             diff = np.setxor1d(final, want)
             assert diff.size <= 2, (name, diff.size)
         tol = 2e-2 if K.dtype == torch.bfloat16 else 1e-4

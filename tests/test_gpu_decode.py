@@ -279,3 +279,42 @@ def test_wave_pipelined_step_matches_single_wave():
     torch.testing.assert_close(o2, o1, rtol=1e-5, atol=1e-6)
     s1, s2 = d1.stats(), d2.stats()
     assert torch.equal(s1.group_b1, s2.group_b1) and torch.equal(s1.cand_pages, s2.cand_pages)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("sink,window", [(4, 64), (0, 100), (37, 1)])
+def test_sink_window_selector_batched(dtype, sink, window):
+    """select_sink_window (selectors.py:164-175) as the base selector of the
+    batched path: candidate tokens, INT4 estimate, top-p and attention vs the
+    oracle on every unit (ragged lengths; one unit short enough to keep all)."""
+    B, H, G, n = 3, 2, 4, 700
+    lengths = [700, 333, 60]
+    cache, batch = _cache(B, H, G, n, dtype, lengths, seed=21, tau=tau_schedule(H, (0.4, 1.5)))
+    p = 0.9
+    dec = TwilightDecoder(cache, "sink_window", p=p, sink=sink, window=window)
+    q = batch.q.contiguous()
+    out = dec.forward(q)
+    torch.cuda.synchronize()
+    bufs = dec.bufs
+    for b in range(B):
+        for h in range(H):
+            u = b * H + h
+            K, V = to_np(cache.unit_keys(b, h)), to_np(cache.unit_values(b, h))
+            want_cand = orc.sink_window_tokens(lengths[b], sink, window)
+            ncand = int(bufs.cand_count[u])
+            pages = bufs.cand_pages[u, :ncand].cpu().numpy()
+            pos = (pages[:, None] * 16 + np.arange(16)).reshape(-1)
+            z_all = bufs.logits[u, :, : ncand * 16].cpu().numpy()
+            valid = np.isfinite(z_all[0])
+            np.testing.assert_array_equal(pos[valid], want_cand)
+            Qn = to_np(q[b, h * G:(h + 1) * G])
+            res = orc.decode_unit(Qn, K, V, selector="sink_window", p=p, sink=sink, window=window,
+                                  logits_override=[z_all[g][valid] for g in range(G)])
+            final = bufs.final_idx[u, : int(bufs.final_count[u])].cpu().numpy()
+            assert np.isin(final, want_cand).all()
+            if not np.array_equal(final, res["final"]):
+                assert np.setxor1d(final, res["final"]).size <= 2  # threshold ties only
+                continue
+            for g in range(G):
+                want = res["out"][g]
+                np.testing.assert_allclose(to_np(out[b, h * G + g]), want, rtol=1e-4, atol=1e-4 * np.abs(want).max())

@@ -71,9 +71,14 @@ def test_cost_model_matches_paper():
 
 def test_unsupported_selectors_fail_loudly():
     with pytest.raises(NotImplementedError):
-        tw.select_sink_window(100, 4, 64)
-    with pytest.raises(NotImplementedError):
         tw.select_channel_pruned(None, None, None, 0.5)
+
+
+def test_select_sink_window_validation():
+    # selectors.py:164-175 argument checks (raised before any device work)
+    for bad in ((0, 1, 1), (10, -1, 3), (10, 0, 0)):
+        with pytest.raises(ValueError):
+            tw.select_sink_window(*bad, device="cpu")
 
 
 def test_pack_codes_known_answers():

@@ -103,10 +103,11 @@ def test_attention_matches_reference(golden):
 
 def test_decode_unit_matches_reference_pipeline(golden):
     for name, c in golden("pipeline").items():
-        budget, p, is_quest, is_frac = c["cfg"]
+        budget, p, kind, is_frac, sink, window = c["cfg"]
         budget = float(budget) if is_frac else int(budget)
-        res = orc.decode_unit(c["Q"], c["K"], c["V"], selector="quest" if is_quest else "full",
-                              budget=budget, p=float(p))
+        selector = ("full", "quest", "sink_window")[int(kind)]
+        res = orc.decode_unit(c["Q"], c["K"], c["V"], selector=selector, budget=budget, p=float(p),
+                              sink=int(sink), window=int(window))
         np.testing.assert_array_equal(res["final"], c["final"], err_msg=name)
         assert res["candidates"].size == c["b0"][0], name
         np.testing.assert_allclose(res["out"], c["out"], rtol=1e-5, atol=1e-6, err_msg=name)
