@@ -219,6 +219,12 @@ def main() -> None:
         for h, f in enumerate(finals):
             assert np.array_equal(f, finals[0]) or G == 1
     np.savez_compressed(os.path.join(OUT, "pipeline.npz"), **pipe)
+
+    # ---------------------------------------------------------- .twlt tensor file (tensorfile.py:61-74)
+    from nucleuskv.tensorfile import write_tensor
+    t = (np.arange(2 * 3 * 5, dtype=np.float32).reshape(2, 3, 5) - 7.25) / 3.0
+    write_tensor(os.path.join(OUT, "ref_tensor.twlt"), t)
+    np.save(os.path.join(OUT, "ref_tensor.npy"), t)
     print("golden vectors written to", OUT)
 
 

@@ -20,6 +20,9 @@ from .selectors import (GroupMap, SelectorConfig, build_selector, group_union, q
                         select_channel_pruned, select_full, select_quest, select_sink_window,
                         top_channels_by_magnitude)
 
+from .tensorfile import (BadMagicError, DimOverflowError, TensorFileError, TruncatedFileError,
+                         VersionMismatchError, load_file_workload, read_tensor, run_file_workload, write_tensor)
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -32,4 +35,6 @@ __all__ = [
     "select_channel_pruned", "select_full", "select_quest", "select_sink_window", "top_channels_by_magnitude",
     "PipelineConfig", "PruneReport", "bypass_config", "memory_overhead", "model_speedup", "run_grouped",
     "run_head", "PagedKVCache", "TwilightDecoder", "DecodeBuffers", "DecodeStats", "pages_for", "__version__",
+    "TensorFileError", "BadMagicError", "VersionMismatchError", "TruncatedFileError", "DimOverflowError",
+    "read_tensor", "write_tensor", "load_file_workload", "run_file_workload",
 ]

@@ -182,3 +182,26 @@ def test_run_grouped_and_run_head_match_reference(golden):
         if np.array_equal(final, want):
             np.testing.assert_allclose(outs.cpu().numpy(), c["out"], rtol=tol, atol=tol * np.abs(c["out"]).max(),
                                        err_msg=name)
+
+
+def test_file_workload_runs_on_the_gpu_path(tmp_path):
+    """workload.py:148-183 file workload (q/k/v .twlt) decoded by run_file_workload
+    vs the oracle's run_grouped restatement per step and KV head."""
+    rng = np.random.default_rng(31)
+    steps, heads, kvh, n = 2, 4, 2, 700
+    bf = lambda x: torch.from_numpy(x.astype(np.float32)).bfloat16().float().numpy()  # noqa: E731
+    q = bf(rng.standard_normal((steps, heads, 128)) * 2.0)
+    k = bf(rng.standard_normal((kvh, n, 128)))
+    v = bf(rng.standard_normal((kvh, n, 128)))
+    for name, a in (("q", q), ("k", k), ("v", v)):
+        tw.write_tensor(tmp_path / f"{name}.twlt", a)
+    cfg = tw.PipelineConfig(selector=tw.SelectorConfig(kind="quest", budget=256),
+                            prune=tw.BinarySearchConfig(p=0.9), group_map=tw.GroupMap(heads // kvh))
+    outs, _ = tw.run_file_workload(tmp_path, cfg)
+    G = heads // kvh
+    for s in range(steps):
+        for h in range(kvh):
+            res = orc.decode_unit(q[s, h * G:(h + 1) * G], k[h], v[h], selector="quest", budget=256, p=0.9)
+            want = res["out"]
+            got = outs[s, h * G:(h + 1) * G].cpu().numpy()
+            np.testing.assert_allclose(got, want, rtol=2e-2, atol=2e-2 * np.abs(want).max())
