@@ -220,6 +220,23 @@ def main() -> None:
             assert np.array_equal(f, finals[0]) or G == 1
     np.savez_compressed(os.path.join(OUT, "pipeline.npz"), **pipe)
 
+    # ---------------------------------------------------------- dynamism summaries (pipeline.py:420-462)
+    from nucleuskv.pipeline import PruneReport, TaggedReport, collect_dynamism
+    dyn = {}
+    tags = [(pr, st, ly, hd) for pr in range(2) for st in range(3) for ly in range(2) for hd in range(4)]
+    b1s = rng.integers(0, 5000, size=len(tags))
+    fields = {f: 0 for f in PruneReport.__dataclass_fields__}
+    reps = [TaggedReport(*t, report=PruneReport(**{**fields, "b1": int(b)})) for t, b in zip(tags, b1s)]
+    stats = collect_dynamism(reps, bins=12)
+    dyn["tags"], dyn["b1"] = np.array(tags), b1s
+    dyn["overall"] = np.array([stats.overall_mean, stats.overall_std])
+    for axis, a in stats.axes.items():
+        dyn[f"{axis}/summary"] = np.array([a.mean, a.std, a.min, a.max])
+        dyn[f"{axis}/groups"] = np.array(sorted(a.group_means.items()), dtype=np.float64)
+        dyn[f"{axis}/edges"] = np.array(a.histogram_edges)
+        dyn[f"{axis}/counts"] = np.array(a.histogram_counts)
+    np.savez_compressed(os.path.join(OUT, "dynamism.npz"), **dyn)
+
     # ---------------------------------------------------------- .twlt tensor file (tensorfile.py:61-74)
     from nucleuskv.tensorfile import write_tensor
     t = (np.arange(2 * 3 * 5, dtype=np.float32).reshape(2, 3, 5) - 7.25) / 3.0

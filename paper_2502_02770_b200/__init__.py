@@ -20,6 +20,8 @@ from .selectors import (GroupMap, SelectorConfig, build_selector, group_union, q
                         select_channel_pruned, select_full, select_quest, select_sink_window,
                         top_channels_by_magnitude)
 
+from .dynamism import (RUN_COLUMNS, AxisSummary, DynamismStats, SweepRow, TaggedReport, collect_dynamism, sweep_p,
+                       tag_decode_stats, write_run_csv)
 from .tensorfile import (BadMagicError, DimOverflowError, TensorFileError, TruncatedFileError,
                          VersionMismatchError, load_file_workload, read_tensor, run_file_workload, write_tensor)
 
@@ -37,4 +39,6 @@ __all__ = [
     "run_head", "PagedKVCache", "TwilightDecoder", "DecodeBuffers", "DecodeStats", "pages_for", "__version__",
     "TensorFileError", "BadMagicError", "VersionMismatchError", "TruncatedFileError", "DimOverflowError",
     "read_tensor", "write_tensor", "load_file_workload", "run_file_workload",
+    "TaggedReport", "AxisSummary", "DynamismStats", "SweepRow", "collect_dynamism", "sweep_p", "tag_decode_stats",
+    "RUN_COLUMNS", "write_run_csv",
 ]

@@ -205,3 +205,26 @@ def test_file_workload_runs_on_the_gpu_path(tmp_path):
             want = res["out"]
             got = outs[s, h * G:(h + 1) * G].cpu().numpy()
             np.testing.assert_allclose(got, want, rtol=2e-2, atol=2e-2 * np.abs(want).max())
+
+
+def test_dynamism_from_a_batched_step_and_sweep_p():
+    from paper_2502_02770_b200.workload import make_batch, tau_schedule
+    B, H, G, n = 2, 2, 4, 600
+    batch = make_batch(B, H, G, n, torch.bfloat16, tau=tau_schedule(H, (0.3, 2.0)), seed=41)
+    cache = tw.PagedKVCache(B, H, G, max_pages=tw.pages_for(n), dtype=torch.bfloat16)
+    cache.prefill(batch.K, batch.V)
+    dec = tw.TwilightDecoder(cache, "quest", budget=256, p=0.9)
+    dec.forward(batch.q.contiguous())
+    tags = tw.tag_decode_stats(dec.stats(), H * G)
+    st = tw.collect_dynamism(tags)
+    b1 = dec.stats().b1.cpu().numpy()
+    assert st.overall_mean == pytest.approx(float(b1.mean()))
+    assert sorted(st.axes["prompt"].group_means) == [0, 1]
+    # p sweep (pipeline.py:465-498): larger p never keeps fewer tokens
+    K = batch.K[0, 0].contiguous()
+    V = batch.V[0, 0].contiguous()
+    items = [(batch.q[0, g], K, V) for g in range(2)]
+    cfg = tw.PipelineConfig(selector=tw.SelectorConfig(kind="quest", budget=256))
+    rows = tw.sweep_p(items, cfg, [0.5, 0.9, 0.99])
+    assert [r.p for r in rows] == [0.5, 0.9, 0.99]
+    assert rows[0].mean_b1 <= rows[1].mean_b1 <= rows[2].mean_b1
