@@ -36,7 +36,8 @@ extern "C" {
 #endif
 
 #define TW_PAGE_SIZE 16
-#define TW_QBLOCK_BYTES 1152
+#define TW_QBLOCK_BYTES 1152  /* 4-bit block; a b-bit block is TW_QBLOCK_BYTES_FOR(b) */
+#define TW_QBLOCK_BYTES_FOR(bits) (256 * (bits) + 128)
 #define TW_DEFAULT_CHUNK 512 /* tokens per sparse-attention work item */
 #define TW_TOPP_BINS 4096        /* top-p histogram bins per query head */
 #define TW_TOPP_MEMBER_CAP 8192  /* crossing-bin members held on chip per unit (more: re-read path) */
@@ -62,7 +63,7 @@ typedef struct tw_paged_kv {
   int32_t max_pages;      /* page_table row length */
   int32_t num_phys_pages; /* pages in the pool */
   int32_t dtype;          /* tw_dtype of K, V, q and kmeta */
-  int32_t reserved;
+  int32_t bits;           /* INT key cache width: 2, 4 or 8 (SUPPORTED_BITS, quantcache.py:38); 0 = 4 */
   void* k_cache;
   void* v_cache;
   uint8_t* kq;

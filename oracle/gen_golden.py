@@ -220,6 +220,31 @@ def main() -> None:
             assert np.array_equal(f, finals[0]) or G == 1
     np.savez_compressed(os.path.join(OUT, "pipeline.npz"), **pipe)
 
+    # ---------------------------------------------------------- 2- and 8-bit caches (SUPPORTED_BITS, quantcache.py:38)
+    qb = {}
+    rng_b = np.random.default_rng(20250207)
+    for bits in (2, 8):
+        for name, K in (("gauss_bf16", bf16_round(rng_b.standard_normal((203, 128)) * 1.3)),
+                        ("wide_f32", (rng_b.standard_normal((70, 128)) *
+                                      np.exp(rng_b.standard_normal((70, 1)) * 2)).astype(np.float32)),
+                        ("constant", np.full((19, 128), 0.625, dtype=np.float32))):
+            cache, _ = nk.build_cache(K, page_size=16, bits=bits)
+            n = K.shape[0]
+            per = 128 * bits // 8
+            qb[f"b{bits}_{name}/K"] = K
+            qb[f"b{bits}_{name}/packed"] = np.concatenate(
+                [np.frombuffer(pg.packed, dtype=np.uint8).reshape(16, per)[: pg.valid_len] for pg in cache.pages])
+            qb[f"b{bits}_{name}/codes"] = np.concatenate(
+                [_unpack_matrix(pg.packed, 16, 128, bits)[: pg.valid_len] for pg in cache.pages])
+            qb[f"b{bits}_{name}/scale"] = np.concatenate([pg.scales[: pg.valid_len] for pg in cache.pages])
+            qb[f"b{bits}_{name}/zero"] = np.concatenate([pg.zeros[: pg.valid_len] for pg in cache.pages])
+            q = bf16_round((rng_b.standard_normal(128) * 1.5).astype(np.float32))
+            idx = np.sort(rng_b.choice(n, size=max(1, n // 2), replace=False))
+            r = nk.estimate_scores(q.astype(K.dtype), cache, nk.TokenSelection.from_indices(idx, n))
+            qb[f"b{bits}_{name}/q"], qb[f"b{bits}_{name}/idx"] = q, idx
+            qb[f"b{bits}_{name}/scores"], qb[f"b{bits}_{name}/bytes"] = r.scores, np.array([r.bytes_touched])
+    np.savez_compressed(os.path.join(OUT, "quant_bits.npz"), **qb)
+
     # ---------------------------------------------------------- dynamism summaries (pipeline.py:420-462)
     from nucleuskv.pipeline import PruneReport, TaggedReport, collect_dynamism
     dyn = {}

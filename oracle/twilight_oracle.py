@@ -71,6 +71,18 @@ def pack_nibbles(codes: np.ndarray) -> np.ndarray:
     return (c[..., 0::2] | (c[..., 1::2] << 4)).astype(np.uint8)
 
 
+def pack_codes_bits(codes: np.ndarray, bits: int) -> np.ndarray:
+    """b-bit codes packed lowest-order field first, 8/b per byte (_pack_matrix,
+    quantcache.py:122-130).  Works on the last axis; returns uint8 (..., d*b/8)."""
+    c = np.asarray(codes, dtype=np.uint16)
+    per = 8 // bits
+    g = c.reshape(c.shape[:-1] + (c.shape[-1] // per, per))
+    out = np.zeros(g.shape[:-1], dtype=np.uint16)
+    for slot in range(per):
+        out |= g[..., slot] << (bits * slot)
+    return out.astype(np.uint8)
+
+
 def unpack_nibbles(packed: np.ndarray) -> np.ndarray:
     """Inverse of pack_nibbles (quantcache.py:132-139, :154-160)."""
     b = np.asarray(packed, dtype=np.uint8)
@@ -351,17 +363,17 @@ def subset_attention(w, V, idx, renormalize: bool) -> np.ndarray:
 # one unit end to end (the hot half of run_grouped / run_head)
 
 
-def prepare_unit(K, page_size: int = PAGE_SIZE):
+def prepare_unit(K, page_size: int = PAGE_SIZE, bits: int = 4):
     """The cache the reference builds once per context (build_cache,
-    quantcache.py:178-235): page bounds + per-row INT4 codes/params."""
+    quantcache.py:178-235): page bounds + per-row b-bit codes/params."""
     lo, hi = page_bounds(K, page_size)
-    codes, scale, zero = quantize_rows(K)
+    codes, scale, zero = quantize_rows(K, bits)
     return lo, hi, codes, scale, zero
 
 
 def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.95,
                 page_size: int = PAGE_SIZE, renormalize: bool = True, logits_override=None, prepared=None,
-                sink: int = 4, window: int = 64):
+                sink: int = 4, window: int = 64, bits: int = 4):
     """run_grouped's hot path for one KV head (pipeline.py:306-360):
 
     per-head Quest (selectors.py:112-132; or select_full :90-94, or
@@ -382,7 +394,7 @@ def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.9
     Q = np.atleast_2d(np.asarray(Q))
     n = K.shape[0]
     G = Q.shape[0]
-    lo, hi, codes, scale, zero = prepared if prepared is not None else prepare_unit(K, page_size)
+    lo, hi, codes, scale, zero = prepared if prepared is not None else prepare_unit(K, page_size, bits)
     if selector == "full":
         head_pages = [np.arange(lo.shape[0]) for _ in range(G)]
     elif selector == "quest":

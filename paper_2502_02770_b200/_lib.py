@@ -21,6 +21,11 @@ TW_SELECT_FULL, TW_SELECT_QUEST, TW_SELECT_SINK_WINDOW = 0, 1, 2
 PAGE_SIZE = 16
 DEFAULT_CHUNK = 512
 QBLOCK_BYTES = 1152
+
+
+def qblock_bytes(bits: int) -> int:
+    """TW_QBLOCK_BYTES_FOR: a (page, KV head) block of b-bit codes + 128 B of fp32 scale/zero."""
+    return 256 * bits + 128
 HEAD_DIM = 128
 TOPP_BINS = 4096          # TW_TOPP_BINS
 TOPP_MEMBER_CAP = 8192    # TW_TOPP_MEMBER_CAP
@@ -42,7 +47,7 @@ class TwPagedKV(ctypes.Structure):
     _fields_ = [
         ("num_seqs", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32), ("group_size", ctypes.c_int32),
         ("head_dim", ctypes.c_int32), ("max_pages", ctypes.c_int32), ("num_phys_pages", ctypes.c_int32),
-        ("dtype", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("dtype", ctypes.c_int32), ("bits", ctypes.c_int32),
         ("k_cache", ctypes.c_void_p), ("v_cache", ctypes.c_void_p), ("kq", ctypes.c_void_p),
         ("kmeta", ctypes.c_void_p), ("kabsmax", ctypes.c_void_p), ("page_table", ctypes.c_void_p),
         ("seq_lens", ctypes.c_void_p),

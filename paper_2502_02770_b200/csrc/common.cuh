@@ -15,6 +15,11 @@ constexpr int kPage = 16;          // tokens per page (SelectorConfig.page_size,
 constexpr int kHeadDim = 128;      // d: Llama-3.1-8B / LongChat-7B head dim
 constexpr int kCodeBytes = kPage * kHeadDim / 2;      // 1024 B of packed nibbles per (page, kv head)
 constexpr int kQBlockBytes = kCodeBytes + kPage * 8;  // + fp32 scale[16] + fp32 zero[16] = 1152 B
+// b-bit caches (quantcache.py:38, SUPPORTED_BITS = 2, 4, 8): the page's codes in the
+// reference's byte layout (lowest-order field first), then the 128 B of parameters
+__host__ __device__ constexpr int code_bytes_for(int bits) { return kPage * kHeadDim * bits / 8; }
+__host__ __device__ constexpr int qblock_bytes_for(int bits) { return code_bytes_for(bits) + kPage * 8; }
+__host__ __device__ inline int cache_bits(const tw_paged_kv& kv) { return kv.bits ? kv.bits : 4; }
 constexpr int kWarp = 32;
 
 // ---------------------------------------------------------------- element types

@@ -20,6 +20,8 @@
 // reference's own byte layout, staged through a per-warp cp.async ring.  The
 // MMA's K order is permuted so the low nibbles of a 32-bit word are one A
 // register and the high nibbles another; q's B fragments use the same order.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace tw {
@@ -72,7 +74,20 @@ __device__ __forceinline__ void load32(const float* p, float (&v)[32]) {
 
 // q fixed point + digit B fragments for the lane's B column (head r), and for
 // the lane's two accumulator columns (heads 2t, 2t+1): sum(q) and 2^-S.
-template <typename T, int G>
+// K slot -> channel map of the lane's A/B fragments (k-slot 4t+i of chunk j,
+// +16 for half 1), chosen per cache width so every A register is a few
+// mask/shift ops on the lane's contiguous code bytes:
+//   4-bit: channel 32t + 8j + 2i + half   (low / high nibbles of word j)
+//   8-bit: channel 32t + 8j + 4 half + i  (words 2j, 2j+1 as they are)
+//   2-bit: channel 32t + 16 half + 4i + j (field j of each byte of word half)
+template <int BITS>
+__device__ __forceinline__ int slot_channel(int t, int j, int half, int i) {
+  if (BITS == 8) return 32 * t + 8 * j + 4 * half + i;
+  if (BITS == 2) return 32 * t + 16 * half + 4 * i + j;
+  return 32 * t + 8 * j + 2 * i + half;
+}
+
+template <typename T, int G, int BITS>
 __device__ __forceinline__ void estimate_prologue(const T* __restrict__ q, int unit, uint32_t (&bd)[kDigits][4][2],
                                                   float (&sq)[2], float (&inv_scale)[2]) {
   const int lane = threadIdx.x & 31, t = lane & 3, r = lane >> 2;
@@ -105,8 +120,7 @@ __device__ __forceinline__ void estimate_prologue(const T* __restrict__ q, int u
       uint32_t dig[kDigits] = {0u, 0u, 0u};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        // k-slot 4t+i (+16 for half 1) <-> channel 32t + 8j + 2i (+1)
-        int x = r < G ? __float2int_rn(qv[8 * j + 2 * i + half] * qscale) : 0;
+        int x = r < G ? __float2int_rn(qv[slot_channel<BITS>(t, j, half, i) - 32 * t] * qscale) : 0;
 #pragma unroll
         for (int k = 0; k < kDigits; ++k) {
           const int d = k + 1 < kDigits ? ((x + 128) & 255) - 128 : x;  // balanced digit, last takes the rest
@@ -122,19 +136,20 @@ __device__ __forceinline__ void estimate_prologue(const T* __restrict__ q, int u
 
 // Persistent warp workers over (unit, 32-candidate-page) items, chunk-major;
 // each warp streams its pages' 1152-B INT4 blocks through a 4-deep cp.async ring.
-template <typename T, int G>
+template <typename T, int G, int BITS>
 __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv, const T* __restrict__ q,
                                                                   tw_decode_buffers buf, int max_chunks,
                                                                   int sw_sink, int sw_window) {
   pdl_wait();
   pdl_trigger();
-  __shared__ __align__(128) uint8_t ring[kEstWarps][kEstStages][kQBlockBytes];
+  constexpr int kBlock = qblock_bytes_for(BITS), kCodes = code_bytes_for(BITS), kRowBytes = kHeadDim * BITS / 8;
+  __shared__ __align__(128) uint8_t ring[kEstWarps][kEstStages][kBlock];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane & 3, r = lane >> 2;
   const int units = kv.num_seqs * kv.num_kv_heads;
   const int T_stride = kv.max_pages * kPage;
   const float inv_sqrt_d = 0.08838834764831845f;  // float32(1/sqrt(128)), as quantcache.py:258
-  uint8_t (*R)[kQBlockBytes] = ring[warp];
+  uint8_t (*R)[kBlock] = ring[warp];
   uint32_t bd[kDigits][4][2];
   float sq[2], isc[2];
   int cur_unit = -1;
@@ -164,13 +179,13 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
     const uint8_t* src_l = kv.kq;
     if (lane < np) {
       lp_l = buf.cand_pages[(size_t)unit * kv.max_pages + c0 + lane];
-      src_l = kv.kq + ((size_t)kv.page_table[(size_t)b * kv.max_pages + lp_l] * kv.num_kv_heads + h) * kQBlockBytes;
+      src_l = kv.kq + ((size_t)kv.page_table[(size_t)b * kv.max_pages + lp_l] * kv.num_kv_heads + h) * kBlock;
     }
     auto issue = [&](int i) {
       const uint8_t* src = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, (unsigned long long)src_l, i));
       uint8_t* dst = R[i % kEstStages];
 #pragma unroll
-      for (int c = lane; c < kQBlockBytes / 16; c += 32) cp_async16(dst + 16 * c, src + 16 * c);
+      for (int c = lane; c < kBlock / 16; c += 32) cp_async16(dst + 16 * c, src + 16 * c);
     };
 #pragma unroll
     for (int i = 0; i < kEstStages - 1; ++i) {
@@ -179,7 +194,7 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
     }
     if (unit != cur_unit) {
       if (cur_unit >= 0) flush_max(cur_unit);
-      estimate_prologue<T, G>(q, unit, bd, sq, isc);
+      estimate_prologue<T, G, BITS>(q, unit, bd, sq, isc);
       cur_unit = unit;
     }
     for (int i = 0; i < np; ++i) {
@@ -188,23 +203,53 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       cp_wait<kEstStages - 1>();
       __syncwarp();
       const uint8_t* pg = R[i % kEstStages];
-      const uint4 lo4 = *reinterpret_cast<const uint4*>(pg + r * 64 + t * 16);
-      const uint4 hi4 = *reinterpret_cast<const uint4*>(pg + (r + 8) * 64 + t * 16);
-      const float pv = reinterpret_cast<const float*>(pg + kCodeBytes)[lane];
+      // the lane's code bytes of rows r and r+8: channels 32t .. 32t+31
+      uint32_t wl[BITS], wh[BITS];
+      if (BITS == 8) {
+        const uint4 a0 = *reinterpret_cast<const uint4*>(pg + r * kRowBytes + t * 32);
+        const uint4 a1 = *reinterpret_cast<const uint4*>(pg + r * kRowBytes + t * 32 + 16);
+        const uint4 b0 = *reinterpret_cast<const uint4*>(pg + (r + 8) * kRowBytes + t * 32);
+        const uint4 b1 = *reinterpret_cast<const uint4*>(pg + (r + 8) * kRowBytes + t * 32 + 16);
+        const uint32_t x[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
+                                b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int k = 0; k < BITS; ++k) { wl[k] = x[k]; wh[k] = x[8 + k]; }
+      } else if (BITS == 4) {
+        const uint4 lo4 = *reinterpret_cast<const uint4*>(pg + r * kRowBytes + t * 16);
+        const uint4 hi4 = *reinterpret_cast<const uint4*>(pg + (r + 8) * kRowBytes + t * 16);
+        const uint32_t x[8] = {lo4.x, lo4.y, lo4.z, lo4.w, hi4.x, hi4.y, hi4.z, hi4.w};
+#pragma unroll
+        for (int k = 0; k < BITS; ++k) { wl[k] = x[k]; wh[k] = x[4 + k]; }
+      } else {
+        const uint2 lo2 = *reinterpret_cast<const uint2*>(pg + r * kRowBytes + t * 8);
+        const uint2 hi2 = *reinterpret_cast<const uint2*>(pg + (r + 8) * kRowBytes + t * 8);
+        wl[0] = lo2.x; wl[1] = lo2.y; wh[0] = hi2.x; wh[1] = hi2.y;
+      }
+      const float pv = reinterpret_cast<const float*>(pg + kCodes)[lane];
       __syncwarp();
       const int lp = __shfl_sync(0xffffffffu, lp_l, i);
       int acc[kDigits][4];
 #pragma unroll
       for (int k = 0; k < kDigits; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0;
-      const uint32_t wl[4] = {lo4.x, lo4.y, lo4.z, lo4.w};
-      const uint32_t wh[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint32_t a[4];
-        a[0] = wl[j] & 0x0F0F0F0Fu;         // row r,   channels 32t+8j + {0,2,4,6}
-        a[1] = wh[j] & 0x0F0F0F0Fu;         // row r+8
-        a[2] = (wl[j] >> 4) & 0x0F0F0F0Fu;  // row r,   channels 32t+8j + {1,3,5,7}
-        a[3] = (wh[j] >> 4) & 0x0F0F0F0Fu;  // row r+8
+        if (BITS == 4) {
+          a[0] = wl[j] & 0x0F0F0F0Fu;         // row r,   channels 32t+8j + {0,2,4,6}
+          a[1] = wh[j] & 0x0F0F0F0Fu;         // row r+8
+          a[2] = (wl[j] >> 4) & 0x0F0F0F0Fu;  // row r,   channels 32t+8j + {1,3,5,7}
+          a[3] = (wh[j] >> 4) & 0x0F0F0F0Fu;  // row r+8
+        } else if (BITS == 8) {
+          a[0] = wl[2 * j];                   // row r,   channels 32t+8j + {0..3}
+          a[1] = wh[2 * j];
+          a[2] = wl[2 * j + 1];               // row r,   channels 32t+8j + {4..7}
+          a[3] = wh[2 * j + 1];
+        } else {
+          a[0] = (wl[0] >> (2 * j)) & 0x03030303u;  // row r, channels 32t + 4i + j
+          a[1] = (wh[0] >> (2 * j)) & 0x03030303u;
+          a[2] = (wl[1] >> (2 * j)) & 0x03030303u;  // row r, channels 32t + 16 + 4i + j
+          a[3] = (wh[1] >> (2 * j)) & 0x03030303u;
+        }
 #pragma unroll
         for (int k = 0; k < kDigits; ++k) mma_u8s8(acc[k], a, bd[k][j][0], bd[k][j][1]);
       }
@@ -259,15 +304,19 @@ __global__ void estimate_tokens_kernel(tw_paged_kv kv, int seq, int kvh, const T
     return;
   }
   const int phys = kv.page_table[(size_t)seq * kv.max_pages + tok / kPage];
-  const uint8_t* qb = kv.kq + ((size_t)phys * kv.num_kv_heads + kvh) * kQBlockBytes;
+  const int bits = cache_bits(kv);
+  const uint8_t* qb = kv.kq + ((size_t)phys * kv.num_kv_heads + kvh) * qblock_bytes_for(bits);
   const int slot = tok % kPage;
-  const uint16_t codes = reinterpret_cast<const uint16_t*>(qb + slot * (kHeadDim / 2))[lane];
-  const float* prm = reinterpret_cast<const float*>(qb + kCodeBytes);
+  const uint8_t* row = qb + slot * (kHeadDim * bits / 8);
+  const uint32_t codes = bits == 8 ? reinterpret_cast<const uint32_t*>(row)[lane]
+                         : bits == 4 ? (uint32_t)reinterpret_cast<const uint16_t*>(row)[lane] : (uint32_t)row[lane];
+  const uint32_t cmask = (1u << bits) - 1u;
+  const float* prm = reinterpret_cast<const float*>(qb + code_bytes_for(bits));
   const double scale = prm[slot], zero = prm[kPage + slot];
   float acc = 0.f;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const float kh = (float)(zero + scale * (double)((codes >> (4 * i)) & 0xF));
+    const float kh = (float)(zero + scale * (double)((codes >> (bits * i)) & cmask));
     acc = fmaf(kh, Elem<T>::to_f(q[4 * lane + i]), acc);
   }
   acc = warp_sum(acc);
@@ -278,29 +327,37 @@ __global__ void estimate_tokens_kernel(tw_paged_kv kv, int seq, int kvh, const T
 
 using namespace tw;
 
-template <typename T, int G>
+template <typename T, int G, int BITS>
 static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, int sw_sink,
                               int sw_window, cudaStream_t stream) {
   const int max_chunks = (kv->max_pages + kEstPagesPerCta - 1) / kEstPagesPerCta;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, estimate_kernel<T, G>, kEstWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, estimate_kernel<T, G, BITS>, kEstWarps * 32, 0);
   const int items = kv->num_seqs * kv->num_kv_heads * max_chunks;
   int grid = sms * persist_cap(per_sm);
   if (grid * kEstWarps > items) grid = (items + kEstWarps - 1) / kEstWarps;
-  launch_pdl(estimate_kernel<T, G>, dim3(grid), dim3(kEstWarps * 32), 0, stream, *kv, q, *buf, max_chunks, sw_sink,
+  launch_pdl(estimate_kernel<T, G, BITS>, dim3(grid), dim3(kEstWarps * 32), 0, stream, *kv, q, *buf, max_chunks, sw_sink,
              sw_window);
 }
 
 template <typename T>
 static int launch_estimate(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, int ss, int sw,
                            cudaStream_t stream) {
+  auto by_bits = [&](auto gtag) {
+    constexpr int GG = decltype(gtag)::value;
+    switch (cache_bits(*kv)) {
+      case 2: launch_estimate_g<T, GG, 2>(kv, q, buf, ss, sw, stream); break;
+      case 8: launch_estimate_g<T, GG, 8>(kv, q, buf, ss, sw, stream); break;
+      default: launch_estimate_g<T, GG, 4>(kv, q, buf, ss, sw, stream); break;
+    }
+  };
   switch (kv->group_size) {
-    case 1: launch_estimate_g<T, 1>(kv, q, buf, ss, sw, stream); break;
-    case 2: launch_estimate_g<T, 2>(kv, q, buf, ss, sw, stream); break;
-    case 4: launch_estimate_g<T, 4>(kv, q, buf, ss, sw, stream); break;
-    case 8: launch_estimate_g<T, 8>(kv, q, buf, ss, sw, stream); break;
+    case 1: by_bits(std::integral_constant<int, 1>{}); break;
+    case 2: by_bits(std::integral_constant<int, 2>{}); break;
+    case 4: by_bits(std::integral_constant<int, 4>{}); break;
+    case 8: by_bits(std::integral_constant<int, 8>{}); break;
     default: return TW_ERR_INVALID;
   }
   return launch_status();

@@ -23,8 +23,12 @@ struct RowQuant {
   double lo;
 };
 
-// Quantize the 128-channel row held 4-per-lane across the warp.
+// Quantize the 128-channel row held 4-per-lane across the warp to BITS-bit
+// codes (levels = 2^BITS - 1), packed lowest-order field first (_pack_matrix,
+// quantcache.py:122-130): 2 bytes per lane for 4-bit, 4 for 8-bit, 1 for 2-bit.
+template <int BITS>
 __device__ __forceinline__ RowQuant quant_row_warp(const float (&k)[4]) {
+  constexpr double kLevels = (double)((1 << BITS) - 1);
   float mn = fminf(fminf(k[0], k[1]), fminf(k[2], k[3]));
   float mx = fmaxf(fmaxf(k[0], k[1]), fmaxf(k[2], k[3]));
 #pragma unroll
@@ -40,12 +44,12 @@ __device__ __forceinline__ RowQuant quant_row_warp(const float (&k)[4]) {
     r.scale = 0.0;
     return r;
   }
-  r.scale = (hi - r.lo) / 15.0;
+  r.scale = (hi - r.lo) / kLevels;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     double c = rint(((double)k[i] - r.lo) / r.scale);
-    c = fmin(fmax(c, 0.0), 15.0);
-    r.packed |= (uint32_t)c << (4 * i);
+    c = fmin(fmax(c, 0.0), kLevels);
+    r.packed |= (uint32_t)c << (BITS * i);
   }
   // nibble order inside the 2 bytes: byte0 = c0 | c1 << 4, byte1 = c2 | c3 << 4
   return r;
@@ -80,16 +84,20 @@ __device__ __forceinline__ void store4<float>(float* p, const float (&o)[4]) {
   *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
 }
 
+template <int BITS>
 __device__ __forceinline__ void write_quant(uint8_t* qblock, int slot, int lane, const RowQuant& r) {
-  reinterpret_cast<uint16_t*>(qblock + slot * (kHeadDim / 2))[lane] = (uint16_t)r.packed;
+  uint8_t* row = qblock + slot * (kHeadDim * BITS / 8);
+  if (BITS == 4) reinterpret_cast<uint16_t*>(row)[lane] = (uint16_t)r.packed;
+  else if (BITS == 8) reinterpret_cast<uint32_t*>(row)[lane] = r.packed;
+  else row[lane] = (uint8_t)r.packed;
   if (lane == 0) {
-    float* prm = reinterpret_cast<float*>(qblock + kCodeBytes);
+    float* prm = reinterpret_cast<float*>(qblock + code_bytes_for(BITS));
     prm[slot] = (float)r.scale;
     prm[kPage + slot] = (float)r.lo;
   }
 }
 
-template <typename T>
+template <typename T, int BITS>
 __global__ void __launch_bounds__(1024) append_kernel(tw_paged_kv kv, const T* __restrict__ k_new,
                                                       const T* __restrict__ v_new,
                                                       const int32_t* positions) {
@@ -110,8 +118,8 @@ __global__ void __launch_bounds__(1024) append_kernel(tw_paged_kv kv, const T* _
   store4<T>(kc + 4 * lane, k);
   store4<T>(vc + 4 * lane, v);
 
-  RowQuant r = quant_row_warp(k);
-  write_quant(kv.kq + ph * kQBlockBytes, slot, lane, r);
+  RowQuant r = quant_row_warp<BITS>(k);
+  write_quant<BITS>(kv.kq + ph * qblock_bytes_for(BITS), slot, lane, r);
 
   // page channel min/max (read-modify-write of the open page)
   T* lo = reinterpret_cast<T*>(kv.kmeta) + ph * 2 * kHeadDim + 4 * lane;
@@ -139,7 +147,7 @@ __global__ void __launch_bounds__(1024) append_kernel(tw_paged_kv kv, const T* _
 
 // Bulk build: block (logical page, sequence), one warp per kv head walking the
 // page's valid rows; also (re)computes the page metadata and the |k| bound.
-template <typename T>
+template <typename T, int BITS>
 __global__ void __launch_bounds__(1024) build_kernel(tw_paged_kv kv) {
   const int lp = blockIdx.x, b = blockIdx.y;
   const int len = kv.seq_lens[b];
@@ -151,7 +159,7 @@ __global__ void __launch_bounds__(1024) build_kernel(tw_paged_kv kv) {
   const size_t ph = (size_t)phys * H + h;
   const int valid = min(kPage, len - lp * kPage);
   const T* kc = reinterpret_cast<const T*>(kv.k_cache) + ph * kPage * kHeadDim;
-  uint8_t* qb = kv.kq + ph * kQBlockBytes;
+  uint8_t* qb = kv.kq + ph * qblock_bytes_for(BITS);
   float mn[4], mx[4], amax = 0.f;
 #pragma unroll
   for (int i = 0; i < 4; ++i) { mn[i] = INFINITY; mx[i] = -INFINITY; }
@@ -164,8 +172,8 @@ __global__ void __launch_bounds__(1024) build_kernel(tw_paged_kv kv) {
       mx[i] = fmaxf(mx[i], k[i]);
       amax = fmaxf(amax, fabsf(k[i]));
     }
-    RowQuant r = quant_row_warp(k);
-    write_quant(qb, s, lane, r);
+    RowQuant r = quant_row_warp<BITS>(k);
+    write_quant<BITS>(qb, s, lane, r);
   }
   T* lo = reinterpret_cast<T*>(kv.kmeta) + ph * 2 * kHeadDim + 4 * lane;
   store4<T>(lo, mn);
@@ -216,31 +224,42 @@ using namespace tw;
 static int check_geometry(const tw_paged_kv* kv) {
   if (!kv || kv->head_dim != kHeadDim || kv->num_kv_heads < 1 || kv->num_kv_heads > 32 ||
       kv->num_seqs < 1 || kv->max_pages < 1 || kv->group_size < 1 || kv->group_size > 8 ||
-      (kv->dtype != TW_F32 && kv->dtype != TW_BF16))
+      (kv->dtype != TW_F32 && kv->dtype != TW_BF16) || (kv->bits != 0 && kv->bits != 2 && kv->bits != 4 &&
+                                                          kv->bits != 8))
     return TW_ERR_INVALID;
   return TW_OK;
 }
+
+#define TW_DISPATCH_BITS(bits_, CALL)                 \
+  switch (bits_) {                                    \
+    case 2: { constexpr int BB = 2; CALL; break; }    \
+    case 8: { constexpr int BB = 8; CALL; break; }    \
+    default: { constexpr int BB = 4; CALL; break; }   \
+  }
 
 extern "C" int tw_quant_append(const tw_paged_kv* kv, const void* k_new, const void* v_new,
                                const int32_t* positions, cudaStream_t stream) {
   if (int s = check_geometry(kv)) return s;
   if (!k_new || !v_new || !positions) return TW_ERR_INVALID;
   dim3 grid(kv->num_seqs), block(32 * kv->num_kv_heads);
-  if (kv->dtype == TW_BF16)
-    append_kernel<__nv_bfloat16><<<grid, block, 0, stream>>>(
-        *kv, (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new, positions);
-  else
-    append_kernel<float><<<grid, block, 0, stream>>>(*kv, (const float*)k_new, (const float*)v_new, positions);
+  if (kv->dtype == TW_BF16) {
+    TW_DISPATCH_BITS(cache_bits(*kv), (append_kernel<__nv_bfloat16, BB><<<grid, block, 0, stream>>>(
+                                           *kv, (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new, positions)))
+  } else {
+    TW_DISPATCH_BITS(cache_bits(*kv), (append_kernel<float, BB><<<grid, block, 0, stream>>>(
+                                           *kv, (const float*)k_new, (const float*)v_new, positions)))
+  }
   return launch_status();
 }
 
 extern "C" int tw_quant_build(const tw_paged_kv* kv, cudaStream_t stream) {
   if (int s = check_geometry(kv)) return s;
   dim3 grid(kv->max_pages, kv->num_seqs), block(32 * kv->num_kv_heads);
-  if (kv->dtype == TW_BF16)
-    build_kernel<__nv_bfloat16><<<grid, block, 0, stream>>>(*kv);
-  else
-    build_kernel<float><<<grid, block, 0, stream>>>(*kv);
+  if (kv->dtype == TW_BF16) {
+    TW_DISPATCH_BITS(cache_bits(*kv), (build_kernel<__nv_bfloat16, BB><<<grid, block, 0, stream>>>(*kv)))
+  } else {
+    TW_DISPATCH_BITS(cache_bits(*kv), (build_kernel<float, BB><<<grid, block, 0, stream>>>(*kv)))
+  }
   return launch_status();
 }
 

@@ -41,7 +41,10 @@ class PagedKVCache:
 
     def __init__(self, num_seqs: int, num_kv_heads: int, group_size: int, max_pages: int,
                  dtype: torch.dtype = torch.bfloat16, device: str | torch.device = "cuda",
-                 page_table: torch.Tensor | None = None, num_phys_pages: int | None = None):
+                 page_table: torch.Tensor | None = None, num_phys_pages: int | None = None, bits: int = 4):
+        if bits not in (2, 4, 8):
+            raise ValueError(f"bits must be one of (2, 4, 8), got {bits}")
+        self.bits = bits
         self.num_seqs, self.num_kv_heads, self.group_size = num_seqs, num_kv_heads, group_size
         self.max_pages = max_pages
         self.dtype = dtype
@@ -58,7 +61,7 @@ class PagedKVCache:
         H = num_kv_heads
         self.k_cache = torch.zeros(num_phys_pages, H, L.PAGE_SIZE, d, dtype=dtype, device=self.device)
         self.v_cache = torch.zeros_like(self.k_cache)
-        self.kq = torch.zeros(num_phys_pages, H, L.QBLOCK_BYTES, dtype=torch.uint8, device=self.device)
+        self.kq = torch.zeros(num_phys_pages, H, L.qblock_bytes(bits), dtype=torch.uint8, device=self.device)
         self.kmeta = torch.zeros(num_phys_pages, H, 2, d, dtype=dtype, device=self.device)
         self.kabsmax = torch.zeros(num_seqs, H, dtype=torch.float32, device=self.device)
         self.seq_lens = torch.zeros(num_seqs, dtype=torch.int32, device=self.device)
@@ -83,6 +86,7 @@ class PagedKVCache:
             s.num_seqs, s.num_kv_heads, s.group_size = self.num_seqs, self.num_kv_heads, self.group_size
             s.head_dim, s.max_pages, s.num_phys_pages = L.HEAD_DIM, self.max_pages, self.num_phys_pages
             s.dtype = L.dtype_code(self.dtype)
+            s.bits = self.bits
             s.k_cache, s.v_cache = L.ptr(self.k_cache), L.ptr(self.v_cache)
             s.kq, s.kmeta, s.kabsmax = L.ptr(self.kq), L.ptr(self.kmeta), L.ptr(self.kabsmax)
             s.page_table, s.seq_lens = L.ptr(self.page_table), L.ptr(self.seq_lens)
@@ -138,12 +142,13 @@ class PagedKVCache:
         return self.v_cache[phys, h].reshape(P * L.PAGE_SIZE, L.HEAD_DIM)[:n]
 
     def unit_quant(self, b: int, h: int):
-        """(packed codes [n, d/2] u8, scale [n] f32, zero [n] f32) of one unit."""
+        """(packed codes [n, d*bits/8] u8, scale [n] f32, zero [n] f32) of one unit."""
         n = int(self.seq_lens[b].item())
         P = pages_for(n)
-        blk = self.kq[self.page_table[b, :P].long(), h]  # [P, 1152]
-        packed = blk[:, :1024].reshape(P * L.PAGE_SIZE, L.HEAD_DIM // 2)[:n]
-        prm = blk[:, 1024:].contiguous().view(torch.float32).view(P, 2, L.PAGE_SIZE)
+        cb = L.PAGE_SIZE * L.HEAD_DIM * self.bits // 8
+        blk = self.kq[self.page_table[b, :P].long(), h]  # [P, qblock_bytes(bits)]
+        packed = blk[:, :cb].reshape(P * L.PAGE_SIZE, L.HEAD_DIM * self.bits // 8)[:n]
+        prm = blk[:, cb:].contiguous().view(torch.float32).view(P, 2, L.PAGE_SIZE)
         scale = prm[:, 0].reshape(-1)[:n]
         zero = prm[:, 1].reshape(-1)[:n]
         return packed, scale, zero

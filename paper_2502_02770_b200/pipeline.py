@@ -118,8 +118,8 @@ def _spearman(a: torch.Tensor, b: torch.Tensor) -> float:
 def _check_cfg(cfg: PipelineConfig) -> None:
     if cfg.selector.kind not in ("full", "quest", "sink_window"):
         raise NotImplementedError(f"selector {cfg.selector.kind!r} is not on the B200 path")
-    if cfg.estimator_bits != 4:
-        raise NotImplementedError("the B200 path estimates with the 4-bit cache (estimator_bits=4)")
+    if cfg.estimator_bits not in (2, 4, 8):
+        raise NotImplementedError("the B200 path estimates with a 2-, 4- or 8-bit cache (estimator_bits)")
     if cfg.selector.page_size != L.PAGE_SIZE:
         raise ValueError("the B200 path uses 16-token pages")
     if cfg.prune.epsilon != 1e-15 or cfg.prune.max_iters != 64:
@@ -138,7 +138,7 @@ def _run(Q: torch.Tensor, keys: torch.Tensor, values: torch.Tensor, cfg: Pipelin
     H = Q.shape[0]
     groups = H // G
     dt = keys.dtype
-    kv = _unit_cache(keys, values.to(dt), group_size=G, num_seqs=groups)
+    kv = _unit_cache(keys, values.to(dt), group_size=G, num_seqs=groups, bits=cfg.estimator_bits)
     if cfg.selector.kind == "quest":
         if cfg.selector.budget is None:
             raise ValueError("selector 'quest' requires a budget")
@@ -191,7 +191,8 @@ def _reports(dec: TwilightDecoder, Q, keys, values, cfg: PipelineConfig, G: int)
                                             attained_true_mass=attained_true, estimator_spearman=rho,
                                             threshold=float(bufs.head_stats[h, 2].item()), iterations=0,
                                             value_norm=value_norm, tokens_selector=n, tokens_estimator=b0,
-                                            tokens_attention=b1, estimator_bytes=b0 * (L.HEAD_DIM // 2 + 4),
+                                            tokens_attention=b1,
+                                            estimator_bytes=b0 * (L.HEAD_DIM * cfg.estimator_bits // 8 + 4),
                                             cost_units=cost, baseline_units=base, modeled_speedup=base / cost)))
     return res
 

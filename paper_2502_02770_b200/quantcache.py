@@ -86,7 +86,7 @@ class PagedQuantKeyCache:
         out = []
         for p in range(pages_for(self.n_tokens)):
             lo, hi = p * 16, min(self.n_tokens, (p + 1) * 16)
-            block = torch.zeros(16, self.d // 2, dtype=torch.uint8, device=packed.device)
+            block = torch.zeros(16, self.d * self.bits // 8, dtype=torch.uint8, device=packed.device)
             block[: hi - lo] = packed[lo:hi]
             sc = torch.zeros(16, dtype=torch.float64, device=packed.device)
             zr = torch.zeros(16, dtype=torch.float64, device=packed.device)
@@ -111,7 +111,7 @@ def _as_cuda_matrix(keys) -> torch.Tensor:
 
 
 def _unit_cache(keys: torch.Tensor, values: torch.Tensor | None = None, group_size: int = 1,
-                num_seqs: int = 1) -> PagedKVCache:
+                num_seqs: int = 1, bits: int = 4) -> PagedKVCache:
     """One KV context as a paged pool.  ``num_seqs`` > 1 makes every sequence
     share the same physical pages (the G-groups of run_grouped)."""
     K = _as_cuda_matrix(keys)
@@ -127,7 +127,8 @@ def _unit_cache(keys: torch.Tensor, values: torch.Tensor | None = None, group_si
     n = K.shape[0]
     P = pages_for(n)
     pt = torch.arange(P, dtype=torch.int32, device=K.device).repeat(num_seqs, 1)
-    cache = PagedKVCache(num_seqs, 1, group_size, P, dtype=dtype, device=K.device, page_table=pt, num_phys_pages=P)
+    cache = PagedKVCache(num_seqs, 1, group_size, P, dtype=dtype, device=K.device, page_table=pt, num_phys_pages=P,
+                         bits=bits)
     V = values if values is not None else torch.zeros_like(K)
     Kp = K.view(1, 1, n, L.HEAD_DIM)
     Vp = torch.as_tensor(V).to(dtype).view(1, 1, n, L.HEAD_DIM)
@@ -211,16 +212,14 @@ def build_cache(keys, page_size: int = 16, bits: int = 4, values=None):
     """quantcache.py:178-235: (PagedQuantKeyCache, PageMetadataTable)."""
     if bits not in SUPPORTED_BITS:
         raise ValueError(f"bits must be one of {SUPPORTED_BITS}, got {bits}")
-    if bits != 4:
-        raise ValueError("the B200 cache is 4-bit (2/8-bit modes are off the accelerated path)")
     if page_size != L.PAGE_SIZE:
         if page_size < 1:
             raise ValueError("page_size must be at least 1")
         raise ValueError("the B200 path uses 16-token pages")
     K = _as_cuda_matrix(keys)
-    kv = _unit_cache(K, values)
+    kv = _unit_cache(K, values, bits=bits)
     n = K.shape[0]
-    return (PagedQuantKeyCache(kv=kv, n_tokens=n, d=K.shape[1], bits=4, page_size=16), PageMetadataTable(kv, n))
+    return (PagedQuantKeyCache(kv=kv, n_tokens=n, d=K.shape[1], bits=bits, page_size=16), PageMetadataTable(kv, n))
 
 
 def estimate_scores(q, cache: PagedQuantKeyCache, candidates: TokenSelection) -> EstimateResult:

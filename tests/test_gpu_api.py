@@ -228,3 +228,44 @@ def test_dynamism_from_a_batched_step_and_sweep_p():
     rows = tw.sweep_p(items, cfg, [0.5, 0.9, 0.99])
     assert [r.p for r in rows] == [0.5, 0.9, 0.99]
     assert rows[0].mean_b1 <= rows[1].mean_b1 <= rows[2].mean_b1
+
+
+@pytest.mark.parametrize("bits", [2, 8])
+def test_two_and_eight_bit_caches(golden, bits):
+    """build_cache(bits) codes / packing / params bit-exact and estimate_scores
+    within fp32 tolerance vs the reference (tests/golden/quant_bits.npz)."""
+    for name, c in golden("quant_bits").items():
+        if int(name[1]) != bits:
+            continue
+        K = as_input(c["K"])
+        cache, _ = tw.build_cache(K, bits=bits)
+        packed, scale, zero = cache.kv.unit_quant(0, 0)
+        np.testing.assert_array_equal(packed.cpu().numpy(), c["packed"], err_msg=name)
+        np.testing.assert_array_equal(scale.cpu().numpy(), c["scale"].astype(np.float32), err_msg=name)
+        np.testing.assert_array_equal(zero.cpu().numpy(), c["zero"].astype(np.float32), err_msg=name)
+        q = cuda(c["q"], K.dtype)
+        r = tw.estimate_scores(q, cache, tw.TokenSelection.from_indices(cuda(c["idx"]).long(), K.shape[0]))
+        assert r.bytes_touched == int(c["bytes"][0])
+        scale_ref = np.abs(c["q"]).sum() * np.abs(c["K"]).max() / np.sqrt(128)
+        np.testing.assert_allclose(r.scores.cpu().numpy(), c["scores"], rtol=0, atol=2e-6 * scale_ref + 1e-6,
+                                   err_msg=name)
+
+
+@pytest.mark.parametrize("bits", [2, 8])
+def test_run_grouped_with_two_and_eight_bit_estimators(bits):
+    """PipelineConfig.estimator_bits = 2 / 8 through the batched kernels vs the
+    oracle restatement of run_grouped with the same cache width."""
+    rng = np.random.default_rng(50 + bits)
+    n, G = 900, 4
+    bf = lambda x: torch.from_numpy(x.astype(np.float32)).bfloat16().float().numpy()  # noqa: E731
+    K, V, Q = bf(rng.standard_normal((n, 128))), bf(rng.standard_normal((n, 128))), bf(rng.standard_normal((G, 128)) * 2)
+    cfg = tw.PipelineConfig(selector=tw.SelectorConfig(kind="quest", budget=300), prune=tw.BinarySearchConfig(p=0.9),
+                            group_map=tw.GroupMap(G), estimator_bits=bits)
+    out, outcomes, reports = tw.run_grouped(cuda(Q, torch.bfloat16), cuda(K, torch.bfloat16), cuda(V, torch.bfloat16), cfg)
+    res = orc.decode_unit(Q, K, V, selector="quest", budget=300, p=0.9, bits=bits)
+    final = outcomes[0].selection.indices.cpu().numpy()
+    assert reports[0].b0 == res["candidates"].size
+    if np.array_equal(final, res["final"]):
+        np.testing.assert_allclose(out.cpu().numpy(), res["out"], rtol=2e-2, atol=2e-2 * np.abs(res["out"]).max())
+    else:
+        assert np.setxor1d(final, res["final"]).size <= 2  # threshold ties only

@@ -318,3 +318,40 @@ def test_sink_window_selector_batched(dtype, sink, window):
             for g in range(G):
                 want = res["out"][g]
                 np.testing.assert_allclose(to_np(out[b, h * G + g]), want, rtol=1e-4, atol=1e-4 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("bits", [2, 8])
+def test_two_and_eight_bit_cache_build_append_estimate(bits):
+    """K1 bulk build and append for 2/8-bit caches bit-exact vs the oracle
+    (quantize_rows + _pack_matrix layout), and the batched INT-b estimate."""
+    B, H, G, n = 2, 2, 4, 640
+    lengths = [640, 401]
+    dtype = torch.bfloat16
+    batch = make_batch(B, H, G, n, dtype, tau=tau_schedule(H, (0.5, 1.0)), seed=60 + bits)
+    cache = PagedKVCache(B, H, G, max_pages=pages_for(n) + 1, dtype=dtype, bits=bits)
+    cache.prefill(batch.K, batch.V, lengths)
+    pos = torch.tensor(lengths, dtype=torch.int32, device="cuda")
+    cache.append(batch.k_new.contiguous(), batch.v_new.contiguous(), pos)  # one appended row per sequence
+    dec = TwilightDecoder(cache, "quest", budget=256, p=0.9)
+    q = batch.q.contiguous()
+    dec.forward(q)
+    torch.cuda.synchronize()
+    for b in range(B):
+        for h in range(H):
+            u = b * H + h
+            K = to_np(cache.unit_keys(b, h))
+            codes, scale, zero = orc.quantize_rows(K, bits)
+            packed, sc, zr = cache.unit_quant(b, h)
+            np.testing.assert_array_equal(packed.cpu().numpy(), orc.pack_codes_bits(codes, bits))
+            np.testing.assert_array_equal(sc.cpu().numpy(), scale.astype(np.float32))
+            np.testing.assert_array_equal(zr.cpu().numpy(), zero.astype(np.float32))
+            ncand = int(dec.bufs.cand_count[u])
+            pages = dec.bufs.cand_pages[u, :ncand].cpu().numpy()
+            cand = orc.pages_to_tokens(pages, K.shape[0])
+            pos_all = (pages[:, None] * 16 + np.arange(16)).reshape(-1)
+            for g in range(G):
+                qh = to_np(q[b, h * G + g])
+                z = dec.bufs.logits[u, g, : ncand * 16].cpu().numpy()[pos_all < K.shape[0]]
+                want = orc.estimate_logits(qh, codes, scale, zero, cand)
+                scale_ref = np.abs(qh).sum() * np.abs(K).max() / np.sqrt(128)
+                np.testing.assert_allclose(z, want, rtol=0, atol=2e-6 * scale_ref + 1e-6)

@@ -111,3 +111,17 @@ def test_decode_unit_matches_reference_pipeline(golden):
         np.testing.assert_array_equal(res["final"], c["final"], err_msg=name)
         assert res["candidates"].size == c["b0"][0], name
         np.testing.assert_allclose(res["out"], c["out"], rtol=1e-5, atol=1e-6, err_msg=name)
+
+
+def test_two_and_eight_bit_caches_match_reference(golden):
+    """SUPPORTED_BITS (quantcache.py:38): codes, packing (_pack_matrix :122-130),
+    params and estimate_scores for the 2- and 8-bit caches."""
+    for name, c in golden("quant_bits").items():
+        bits = int(name[1])
+        codes, scale, zero = orc.quantize_rows(c["K"], bits)
+        np.testing.assert_array_equal(codes, c["codes"], err_msg=name)
+        np.testing.assert_array_equal(orc.pack_codes_bits(codes, bits), c["packed"], err_msg=name)
+        np.testing.assert_array_equal(scale, c["scale"], err_msg=name)
+        np.testing.assert_array_equal(zero, c["zero"], err_msg=name)
+        z = orc.estimate_logits(c["q"], codes, scale, zero, c["idx"])
+        np.testing.assert_allclose(z, c["scores"], rtol=1e-6, atol=1e-6, err_msg=name)
