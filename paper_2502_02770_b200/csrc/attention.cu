@@ -12,7 +12,7 @@
 // independent worker walking that list; split units are merged afterwards
 // (split-KV log-sum-exp) by a small parallel merge kernel.
 //
-// Per warp: a 3-stage cp.async (LDGSTS, 16 B per lane) ring of 16-row K/V
+// Per warp: a 2-stage cp.async (LDGSTS, 16 B per lane) ring of 16-row K/V
 // tiles, XOR-swizzled so ldmatrix is bank-conflict free.  (Measured on B200,
 // tools/tma_bench.cu: cp.async.bulk costs ~70 cycles per copy per issuing
 // CTA, i.e. ~1 TB/s for 256-B row gathers at one CTA/SM, while LDGSTS moves
@@ -29,7 +29,7 @@ constexpr int kAttWarps = 4;            // warps (= independent workers) per CTA
 constexpr int kAttThreads = kAttWarps * 32;
 constexpr int kTile = 16;               // rows per stage
 #ifndef TW_ATT_STAGES
-#define TW_ATT_STAGES 3
+#define TW_ATT_STAGES 2
 #endif
 constexpr int kNS = TW_ATT_STAGES;      // stages per warp
 constexpr int kMaxChunk = 512;          // tokens per work item (upper bound)
