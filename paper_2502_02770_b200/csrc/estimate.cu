@@ -134,6 +134,58 @@ __device__ __forceinline__ void estimate_prologue(const T* __restrict__ q, int u
   }
 }
 
+// G <= 4: the digit columns are packed -- MMA 1 holds digits 0 and 1 of every
+// head (B column 2g + d), MMA 2 digit 2 (column 2g; 2g + 1 is zero) -- so a page
+// takes 8 integer MMAs instead of 12 and lane (t, r) ends with head t's rows
+// r and r + 8.  The digit sums are combined in the same order as the unpacked
+// path, so the logits are bit-identical.
+template <typename T, int G, int BITS>
+__device__ __forceinline__ void estimate_prologue_packed(const T* __restrict__ q, int unit, uint32_t (&b1)[4][2],
+                                                         uint32_t (&b2)[4][2], float& sq, float& inv_scale) {
+  const int lane = threadIdx.x & 31, t = lane & 3, r = lane >> 2;
+  const int hb = r >> 1, dsel = r & 1;  // this lane's B column r: head hb, digit dsel (MMA 1) / 2 (MMA 2, even r)
+  int Sb = 0;
+  sq = 0.f;
+  inv_scale = 1.f;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const T* qg = q + ((size_t)unit * G + g) * kHeadDim + 4 * lane;
+    float v0, v1, v2, v3;
+    load4(qg, v0, v1, v2, v3);
+    float s = (v0 + v1) + (v2 + v3);
+    float m = fmaxf(fmaxf(fabsf(v0), fabsf(v1)), fmaxf(fabsf(v2), fabsf(v3)));
+    s = warp_sum(s);
+    m = warp_max(m);
+    const int S = m > 0.f ? min(21 - ilogbf(m), 126) : 0;
+    if (g == hb) Sb = S;
+    if (g == t) { sq = s; inv_scale = ldexpf(1.f, -S); }
+  }
+  float qv[32];
+  load32(q + ((size_t)unit * G + (hb < G ? hb : 0)) * kHeadDim + 32 * t, qv);
+  const float qscale = ldexpf(1.f, Sb);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t d1 = 0u, d2 = 0u;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int x = hb < G ? __float2int_rn(qv[slot_channel<BITS>(t, j, half, i) - 32 * t] * qscale) : 0;
+        int dig[kDigits];
+#pragma unroll
+        for (int k = 0; k < kDigits; ++k) {
+          dig[k] = k + 1 < kDigits ? ((x + 128) & 255) - 128 : x;
+          x = (x - dig[k]) >> 8;
+        }
+        d1 |= ((uint32_t)(dsel ? dig[1] : dig[0]) & 255u) << (8 * i);
+        d2 |= ((uint32_t)(dsel ? 0 : dig[2]) & 255u) << (8 * i);
+      }
+      b1[j][half] = d1;
+      b2[j][half] = d2;
+    }
+  }
+}
+
 // Persistent warp workers over (unit, 32-candidate-page) items, chunk-major;
 // each warp streams its pages' 1152-B INT4 blocks through a 4-deep cp.async ring.
 template <typename T, int G, int BITS>
@@ -150,11 +202,22 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
   const int T_stride = kv.max_pages * kPage;
   const float inv_sqrt_d = 0.08838834764831845f;  // float32(1/sqrt(128)), as quantcache.py:258
   uint8_t (*R)[kBlock] = ring[warp];
-  uint32_t bd[kDigits][4][2];
+  constexpr bool kPacked = G <= 4;
+  uint32_t bd[kPacked ? 1 : kDigits][4][2];
+  uint32_t pb1[4][2], pb2[4][2];
   float sq[2], isc[2];
   int cur_unit = -1;
   float run_max[2] = {-INFINITY, -INFINITY};
   auto flush_max = [&](int u) {
+    if constexpr (kPacked) {
+      float mx = run_max[0];
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      if (r == 0 && t < G && mx > -INFINITY) atomicMax(buf.head_max + (size_t)u * G + t, f2key(mx));
+      run_max[0] = -INFINITY;
+      return;
+    }
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       float mx = run_max[e];
@@ -194,7 +257,8 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
     }
     if (unit != cur_unit) {
       if (cur_unit >= 0) flush_max(cur_unit);
-      estimate_prologue<T, G, BITS>(q, unit, bd, sq, isc);
+      if constexpr (kPacked) estimate_prologue_packed<T, G, BITS>(q, unit, pb1, pb2, sq[0], isc[0]);
+      else estimate_prologue<T, G, BITS>(q, unit, reinterpret_cast<uint32_t (&)[kDigits][4][2]>(bd), sq, isc);
       cur_unit = unit;
     }
     for (int i = 0; i < np; ++i) {
@@ -228,9 +292,9 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       const float pv = reinterpret_cast<const float*>(pg + kCodes)[lane];
       __syncwarp();
       const int lp = __shfl_sync(0xffffffffu, lp_l, i);
-      int acc[kDigits][4];
+      int acc[kPacked ? 2 : kDigits][4];
 #pragma unroll
-      for (int k = 0; k < kDigits; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0;
+      for (int k = 0; k < (kPacked ? 2 : kDigits); ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint32_t a[4];
@@ -250,23 +314,45 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
           a[2] = (wl[1] >> (2 * j)) & 0x03030303u;  // row r, channels 32t + 16 + 4i + j
           a[3] = (wh[1] >> (2 * j)) & 0x03030303u;
         }
+        if constexpr (kPacked) {
+          mma_u8s8(acc[0], a, pb1[j][0], pb1[j][1]);
+          mma_u8s8(acc[1], a, pb2[j][0], pb2[j][1]);
+        } else {
 #pragma unroll
-        for (int k = 0; k < kDigits; ++k) mma_u8s8(acc[k], a, bd[k][j][0], bd[k][j][1]);
+          for (int k = 0; k < kDigits; ++k)
+            mma_u8s8(acc[k], a, reinterpret_cast<uint32_t (&)[kDigits][4][2]>(bd)[k][j][0],
+                     reinterpret_cast<uint32_t (&)[kDigits][4][2]>(bd)[k][j][1]);
+        }
       }
       // ---- epilogue: rows r and r+8, heads 2t and 2t+1
       const float sc_r = __shfl_sync(0xffffffffu, pv, r), sc_r8 = __shfl_sync(0xffffffffu, pv, r + 8);
       const float z_r = __shfl_sync(0xffffffffu, pv, 16 + r), z_r8 = __shfl_sync(0xffffffffu, pv, 24 + r);
       float d[4];
+      if constexpr (kPacked) {  // head t: digits 0, 1 in acc[0] columns (2t, 2t+1), digit 2 in acc[1] column 2t
+        d[0] = fmaf((float)acc[1][0], 65536.f, fmaf((float)acc[0][1], 256.f, (float)acc[0][0])) * isc[0];
+        d[2] = fmaf((float)acc[1][2], 65536.f, fmaf((float)acc[0][3], 256.f, (float)acc[0][2])) * isc[0];
+        d[1] = d[3] = 0.f;
+      } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        d[e] = fmaf((float)acc[2][e], 65536.f, fmaf((float)acc[1][e], 256.f, (float)acc[0][e])) * isc[e & 1];
+        for (int e = 0; e < 4; ++e)
+          d[e] = fmaf((float)acc[2][e], 65536.f, fmaf((float)acc[1][e], 256.f, (float)acc[0][e])) * isc[e & 1];
+      }
       const int tok_r = lp * kPage + r;
       // sink-window selection (selectors.py:164-175): tokens between the sink and the window are not candidates
       const bool swm = sw_window >= 0 && sw_sink + sw_window < n;
       const bool v_r = tok_r < n && (!swm || tok_r < sw_sink || tok_r >= n - sw_window);
       const bool v_r8 = tok_r + 8 < n && (!swm || tok_r + 8 < sw_sink || tok_r + 8 >= n - sw_window);
       const int ci = c0 + i;
-      if (2 * t < G) {
+      if constexpr (kPacked) {
+        if (t < G) {
+          const float l0 = v_r ? fmaf(sc_r, d[0], z_r * sq[0]) * inv_sqrt_d : -INFINITY;
+          const float l1 = v_r8 ? fmaf(sc_r8, d[2], z_r8 * sq[0]) * inv_sqrt_d : -INFINITY;
+          float* lg = buf.logits + ((size_t)unit * G + t) * T_stride + (size_t)ci * kPage;
+          lg[r] = l0;
+          lg[r + 8] = l1;
+          run_max[0] = fmaxf(run_max[0], fmaxf(l0, l1));
+        }
+      } else if (2 * t < G) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int g = 2 * t + e;
