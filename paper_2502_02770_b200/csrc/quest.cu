@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_kernel(tw_paged_kv
 // Per warp: 16-page tiles (16 x 512 B, XOR-swizzled rows) through a 3-stage
 // cp.async ring; one ldmatrix.x4 + one MMA per page-tile k-step.
 #ifndef TW_QM_STAGES
-#define TW_QM_STAGES 3
+#define TW_QM_STAGES 2
 #endif
 constexpr int kQmStages = TW_QM_STAGES;
 
