@@ -124,6 +124,10 @@ struct StateMMA {
   float o[8][4];  // O^T: m-tile i (channels 16i..16i+15) x heads (2t, 2t+1)
 };
 
+// PACKED (G <= 4): the P split's hi and lo halves share one PV MMA as
+// columns (2g, 2g+1) of head g, so the PV product takes 8 MMAs per tile
+// instead of 16 and lane (t, r) accumulates head t (o = hi column + lo column).
+template <bool PACKED>
 __device__ __forceinline__ void consume_mma(StateMMA& st, const uint32_t (&qb)[8][2], const char* K,
                                             const char* V, int rows) {
   const int lane = threadIdx.x & 31;
@@ -161,33 +165,64 @@ __device__ __forceinline__ void consume_mma(StateMMA& st, const uint32_t (&qb)[8
     st.l[c] = st.l[c] * alpha[c] + ps;
     st.m[c] = mn;
   }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    st.o[i][0] *= alpha[0];
-    st.o[i][1] *= alpha[1];
-    st.o[i][2] *= alpha[0];
-    st.o[i][3] *= alpha[1];
-  }
-  // P^T B fragments from the S^T accumulators (rows 2t,2t+1 | 2t+8,2t+9 of head g)
-  const int g = lane >> 2;
-  const int srcA = 8 * t + (g >> 1), srcB = srcA + 4;
-  const uint32_t selp = (g & 1) ? 0x7632u : 0x5410u;
   const uint32_t h01 = pack_bf16(s[0], s[1]), h23 = pack_bf16(s[2], s[3]);
   const __nv_bfloat162 hb01 = *reinterpret_cast<const __nv_bfloat162*>(&h01);
   const __nv_bfloat162 hb23 = *reinterpret_cast<const __nv_bfloat162*>(&h23);
   const uint32_t l01 = pack_bf16(s[0] - __low2float(hb01), s[1] - __high2float(hb01));
   const uint32_t l23 = pack_bf16(s[2] - __low2float(hb23), s[3] - __high2float(hb23));
-  const uint32_t bh0 = __byte_perm(__shfl_sync(0xffffffffu, h01, srcA), __shfl_sync(0xffffffffu, h01, srcB), selp);
-  const uint32_t bh1 = __byte_perm(__shfl_sync(0xffffffffu, h23, srcA), __shfl_sync(0xffffffffu, h23, srcB), selp);
-  const uint32_t bl0 = __byte_perm(__shfl_sync(0xffffffffu, l01, srcA), __shfl_sync(0xffffffffu, l01, srcB), selp);
-  const uint32_t bl1 = __byte_perm(__shfl_sync(0xffffffffu, l23, srcA), __shfl_sync(0xffffffffu, l23, srcB), selp);
   const int vrow = (q8 >> 1) * 8 + rr;
+  if constexpr (PACKED) {
+    // this lane's PV column r = (head r >> 1, hi | lo); its accumulators hold head t
+    const int hb = r >> 1;
+    const int srcA = 8 * t + (hb >> 1), srcB = srcA + 4;
+    const uint32_t selp = (hb & 1) ? 0x7632u : 0x5410u;
+    const bool lo = r & 1;
+    const uint32_t ha = __shfl_sync(0xffffffffu, h01, srcA), hbv = __shfl_sync(0xffffffffu, h01, srcB);
+    const uint32_t la = __shfl_sync(0xffffffffu, l01, srcA), lb = __shfl_sync(0xffffffffu, l01, srcB);
+    const uint32_t ha8 = __shfl_sync(0xffffffffu, h23, srcA), hb8 = __shfl_sync(0xffffffffu, h23, srcB);
+    const uint32_t la8 = __shfl_sync(0xffffffffu, l23, srcA), lb8 = __shfl_sync(0xffffffffu, l23, srcB);
+    const uint32_t b0 = __byte_perm(lo ? la : ha, lo ? lb : hbv, selp);
+    const uint32_t b1 = __byte_perm(lo ? la8 : ha8, lo ? lb8 : hb8, selp);
+    // rescale head t's accumulators by its alpha (held by lanes t' = t >> 1, component t & 1)
+    const int src = 4 * r + (t >> 1);
+    const float a0 = __shfl_sync(0xffffffffu, alpha[0], src), a1 = __shfl_sync(0xffffffffu, alpha[1], src);
+    const float at = (t & 1) ? a1 : a0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    uint32_t a[4];
-    ldsm_x4_t(a, V + swz(vrow, 2 * i + (q8 & 1)));
-    mma16816(st.o[i], a, bh0, bh1);
-    mma16816(st.o[i], a, bl0, bl1);
+    for (int i = 0; i < 8; ++i) {
+      st.o[i][0] *= at;
+      st.o[i][1] *= at;
+      st.o[i][2] *= at;
+      st.o[i][3] *= at;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t a[4];
+      ldsm_x4_t(a, V + swz(vrow, 2 * i + (q8 & 1)));
+      mma16816(st.o[i], a, b0, b1);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      st.o[i][0] *= alpha[0];
+      st.o[i][1] *= alpha[1];
+      st.o[i][2] *= alpha[0];
+      st.o[i][3] *= alpha[1];
+    }
+    // P^T B fragments from the S^T accumulators (rows 2t,2t+1 | 2t+8,2t+9 of head g)
+    const int g = lane >> 2;
+    const int srcA = 8 * t + (g >> 1), srcB = srcA + 4;
+    const uint32_t selp = (g & 1) ? 0x7632u : 0x5410u;
+    const uint32_t bh0 = __byte_perm(__shfl_sync(0xffffffffu, h01, srcA), __shfl_sync(0xffffffffu, h01, srcB), selp);
+    const uint32_t bh1 = __byte_perm(__shfl_sync(0xffffffffu, h23, srcA), __shfl_sync(0xffffffffu, h23, srcB), selp);
+    const uint32_t bl0 = __byte_perm(__shfl_sync(0xffffffffu, l01, srcA), __shfl_sync(0xffffffffu, l01, srcB), selp);
+    const uint32_t bl1 = __byte_perm(__shfl_sync(0xffffffffu, l23, srcA), __shfl_sync(0xffffffffu, l23, srcB), selp);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t a[4];
+      ldsm_x4_t(a, V + swz(vrow, 2 * i + (q8 & 1)));
+      mma16816(st.o[i], a, bh0, bh1);
+      mma16816(st.o[i], a, bl0, bl1);
+    }
   }
 }
 
@@ -295,10 +330,37 @@ __global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const
           for (int z = lane; z < (kTile - rows) * 16; z += 32) vz[z] = make_uint4(0, 0, 0, 0);
           __syncwarp();
         }
-        consume_mma(st, qb, reinterpret_cast<const char*>(&W.k[slot][0][0]),
-                    reinterpret_cast<const char*>(&W.v[slot][0][0]), rows);
+        consume_mma<(G <= 4)>(st, qb, reinterpret_cast<const char*>(&W.k[slot][0][0]),
+                              reinterpret_cast<const char*>(&W.v[slot][0][0]), rows);
         __syncwarp();
       }
+      if constexpr (G <= 4) {
+        // packed: lane (t, r) holds head t (hi + lo columns) for channels 16i + r (+8); its
+        // softmax state sits in lanes t' = t >> 1, component t & 1
+        const int src = 4 * r + (t >> 1);
+        const float m0 = __shfl_sync(0xffffffffu, st.m[0], src), m1 = __shfl_sync(0xffffffffu, st.m[1], src);
+        const float l0 = __shfl_sync(0xffffffffu, st.l[0], src), l1 = __shfl_sync(0xffffffffu, st.l[1], src);
+        const float mt = (t & 1) ? m1 : m0, lt = (t & 1) ? l1 : l0;
+        if (t < G) {
+          const float inv = lt > 0.f ? 1.f / lt : 0.f;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int c0 = 16 * i + r;
+            const float o0 = st.o[i][0] + st.o[i][1], o8 = st.o[i][2] + st.o[i][3];
+            if (single) {
+              out[((size_t)d.unit * G + t) * kHeadDim + c0] = o0 * inv;
+              out[((size_t)d.unit * G + t) * kHeadDim + c0 + 8] = o8 * inv;
+            } else {
+              part[t * (kHeadDim + 2) + c0] = o0;
+              part[t * (kHeadDim + 2) + c0 + 8] = o8;
+            }
+          }
+          if (!single && r == 0) {
+            part[t * (kHeadDim + 2) + kHeadDim] = mt;
+            part[t * (kHeadDim + 2) + kHeadDim + 1] = lt;
+          }
+        }
+      } else {
       // emit: lane holds heads 2t, 2t+1 for channels 16i + r (+8)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -321,6 +383,7 @@ __global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const
             part[g2 * (kHeadDim + 2) + kHeadDim + 1] = st.l[c];
           }
         }
+      }
       }
     } else {
       float qf[G][4];
