@@ -343,10 +343,14 @@ def run_ours(args, cfg):
     dense_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
 
     # --- end to end through the C-ABI step with host buffers (pinned), H2D + D2H inside the timed region
-    q_h = q.cpu().pin_memory()
-    k_h, v_h = k_new.cpu().pin_memory(), v_new.cpu().pin_memory()
+    # the step's inputs travel as ONE pinned staging buffer (q | k_new | v_new), one H2D copy per step
+    nq, nk = q.numel(), k_new.numel()
+    inp_h = torch.cat([q.reshape(-1), k_new.reshape(-1), v_new.reshape(-1)]).cpu().pin_memory()
+    inp_d = torch.empty_like(inp_h, device=q.device)
+    q_d = inp_d[:nq].view(q.shape)
+    k_d = inp_d[nq:nq + nk].view(k_new.shape)
+    v_d = inp_d[nq + nk:].view(v_new.shape)
     out_h = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-    q_d, k_d, v_d = q.clone(), k_new.clone(), v_new.clone()
     e2e_graphs = []
     for i in range(L):
         g = torch.cuda.CUDAGraph()
@@ -354,17 +358,13 @@ def run_ours(args, cfg):
             decs[i].step(q_d, k_d, v_d, positions, out)
         e2e_graphs.append(g)
     for i in range(args.warmup):  # (every input copied: a garbage k_new would poison the |k| bound)
-        q_d.copy_(q_h, non_blocking=True)
-        k_d.copy_(k_h, non_blocking=True)
-        v_d.copy_(v_h, non_blocking=True)
+        inp_d.copy_(inp_h, non_blocking=True)
         e2e_graphs[i % L].replay()
     torch.cuda.synchronize()
     barrier(world)
     e0.record(stream)
     for i in range(args.steps):
-        q_d.copy_(q_h, non_blocking=True)
-        k_d.copy_(k_h, non_blocking=True)
-        v_d.copy_(v_h, non_blocking=True)
+        inp_d.copy_(inp_h, non_blocking=True)
         e2e_graphs[i % L].replay()
         if gathered is not None:
             import torch.distributed as dist
