@@ -229,10 +229,7 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       run_max[e] = -INFINITY;
     }
   };
-  // the next item's index is fetched while this one streams (its atomic's latency is hidden)
-  int it = warp_fetch(buf.counters + 3);
-  for (int next_raw = 0; it < units * max_chunks; it = __shfl_sync(0xffffffffu, next_raw, 0)) {
-    if (lane == 0) next_raw = (int)atomicAdd(buf.counters + 3, 1u);
+  for (int it = warp_fetch(buf.counters + 3); it < units * max_chunks; it = warp_fetch(buf.counters + 3)) {
     const int unit = it % units;  // chunk-major: non-empty items come first, spread over all warps
     const int c0 = (it / units) * kEstPagesPerCta;
     const int ncand = buf.cand_count[unit];
