@@ -43,7 +43,10 @@ extern "C" int tw_debug_strace(unsigned long long* host_out) {
 namespace tw {
 
 constexpr int kSelThreads = 512;
-constexpr int kFilterPagesPerCta = 64;
+#ifndef TW_QF_ITEM
+#define TW_QF_ITEM 64
+#endif
+constexpr int kFilterPagesPerCta = TW_QF_ITEM;
 
 // ---------------------------------------------------------------- filter pass
 
