@@ -436,19 +436,20 @@ __global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const
   }
 }
 
-// Merge the split-KV partials of every unit with more than one item: one CTA
-// per unit; item weights exp(m_i - M) first, then each warp sums a strided
-// subset of the items with float4 loads (all independent, so the loads of a
-// warp are in flight together) and the warps' sums are added in shared memory.
+// Merge the split-KV partials of every unit with more than one item
+// (log-sum-exp over the union of the items, attention.py:130-135): one CTA of
+// 128 threads per (unit, head).  Thread i < n loads item i's (m, l) -- one
+// round of loads for every item -- the CTA reduces the max and the weights,
+// then thread c sums item outputs o_ic with all loads of a batch in flight.
 template <int G, bool DENSE>
-__global__ void __launch_bounds__(256) merge_kernel(tw_paged_kv kv, tw_decode_buffers buf, float* __restrict__ out,
-                                                    int chunk, int max_chunks) {
+__global__ void __launch_bounds__(kHeadDim) merge_kernel(tw_paged_kv kv, tw_decode_buffers buf, float* __restrict__ out,
+                                                         int chunk, int max_chunks) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float w[2048];
-  __shared__ float Lsum[8];
-  __shared__ __align__(16) float red[8][G * kHeadDim];
-  const int unit = blockIdx.x;
+  constexpr int kMaxItems = 1024;
+  __shared__ float e_s[kMaxItems];
+  __shared__ float red[kHeadDim / 32], red2[kHeadDim / 32];
+  const int unit = blockIdx.x / G, g = blockIdx.x % G, c = threadIdx.x, lane = c & 31, warp = c >> 5;
   int first, n;
   if (DENSE) {
     const int len = kv.seq_lens[unit / kv.num_kv_heads];
@@ -459,57 +460,45 @@ __global__ void __launch_bounds__(256) merge_kernel(tw_paged_kv kv, tw_decode_bu
     n = buf.unit_items[2 * unit + 1];
   }
   if (n <= 1) return;
-  const float* P = buf.partials;
   constexpr int kStride = G * (kHeadDim + 2);
-  for (int x = threadIdx.x; x < G * n; x += blockDim.x) {
-    const int g = x / n, i = x % n;
-    w[x] = P[(size_t)(first + i) * kStride + g * (kHeadDim + 2) + kHeadDim];
+  const float* P = buf.partials + (size_t)first * kStride + g * (kHeadDim + 2);
+  // item maxima (n <= kMaxItems: tw_max_work_items bounds the items of one unit)
+  float mloc = -INFINITY;
+  for (int i = c; i < n; i += kHeadDim) {
+    const float mi = P[(size_t)i * kStride + kHeadDim];
+    e_s[i] = mi;
+    mloc = fmaxf(mloc, mi);
   }
+  mloc = warp_max(mloc);
+  if (lane == 0) red[warp] = mloc;
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int g = warp; g < G; g += blockDim.x / 32) {
-    float M = -INFINITY;
-    for (int i = lane; i < n; i += 32) M = fmaxf(M, w[g * n + i]);
-    M = warp_max(M);
-    float L = 0.f;
-    for (int i = lane; i < n; i += 32) {
-      const float mi = w[g * n + i];
-      const float e = mi == -INFINITY ? 0.f : __expf(mi - M);
-      L += e * P[(size_t)(first + i) * kStride + g * (kHeadDim + 2) + kHeadDim + 1];
-      w[g * n + i] = e;
-    }
-    L = warp_sum(L);
-    if (lane == 0) Lsum[g] = L;
+  float M = red[0];
+#pragma unroll
+  for (int w = 1; w < kHeadDim / 32; ++w) M = fmaxf(M, red[w]);
+  float lloc = 0.f;
+  for (int i = c; i < n; i += kHeadDim) {
+    const float mi = e_s[i];
+    const float e = mi == -INFINITY ? 0.f : __expf(mi - M);
+    e_s[i] = e;
+    lloc = fmaf(e, P[(size_t)i * kStride + kHeadDim + 1], lloc);
   }
+  lloc = warp_sum(lloc);
+  if (lane == 0) red2[warp] = lloc;
   __syncthreads();
-  // lane owns channels 4*lane..4*lane+3 of every head; warp sums items warp, warp+8, ...
-  float acc[G][4];
+  float L = 0.f;
 #pragma unroll
-  for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
-  for (int i = warp; i < n; i += 8) {
-    const float* pi = P + (size_t)(first + i) * kStride;
+  for (int w = 0; w < kHeadDim / 32; ++w) L += red2[w];
+  float O = 0.f;
+  int i = 0;
+  for (; i + 16 <= n; i += 16) {
+    float o[16];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float wi = w[g * n + i];
-      const float2 a = *reinterpret_cast<const float2*>(pi + g * (kHeadDim + 2) + 4 * lane);
-      const float2 b = *reinterpret_cast<const float2*>(pi + g * (kHeadDim + 2) + 4 * lane + 2);
-      acc[g][0] = fmaf(wi, a.x, acc[g][0]);
-      acc[g][1] = fmaf(wi, a.y, acc[g][1]);
-      acc[g][2] = fmaf(wi, b.x, acc[g][2]);
-      acc[g][3] = fmaf(wi, b.y, acc[g][3]);
-    }
+    for (int k = 0; k < 16; ++k) o[k] = P[(size_t)(i + k) * kStride + c];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) O = fmaf(e_s[i + k], o[k], O);
   }
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-    *reinterpret_cast<float4*>(&red[warp][g * kHeadDim + 4 * lane]) = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
-  __syncthreads();
-  for (int x = threadIdx.x; x < G * kHeadDim; x += blockDim.x) {
-    float O = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) O += red[k][x];
-    const float L = Lsum[x / kHeadDim];
-    out[(size_t)unit * G * kHeadDim + x] = L > 0.f ? O / L : 0.f;
-  }
+  for (; i < n; ++i) O = fmaf(e_s[i], P[(size_t)i * kStride + c], O);
+  out[((size_t)unit * G + g) * kHeadDim + c] = L > 0.f ? O / L : 0.f;
 }
 
 }  // namespace tw
@@ -524,6 +513,7 @@ static int launch_attn(const tw_paged_kv* kv, const T* q, const tw_decode_buffer
   const int max_chunks = (T_tokens + chunk - 1) / chunk;
   const int total = DENSE ? units * max_chunks : (int)buf->max_items;
   if (chunk > kMaxChunk || chunk % kTile != 0) return TW_ERR_INVALID;
+  if (max_chunks > 1024) return TW_ERR_INVALID;  // items of one unit fit the merge kernel's weights
   if ((int64_t)max_chunks * G > 2048) return TW_ERR_INVALID;  // merge weights fit shared memory
   if (DENSE && (int64_t)units * max_chunks > buf->max_items) return TW_ERR_INVALID;
   int dev = 0, sms = 148;
@@ -538,7 +528,7 @@ static int launch_attn(const tw_paged_kv* kv, const T* q, const tw_decode_buffer
   if (DENSE && grid * kAttWarps > total) grid = (total + kAttWarps - 1) / kAttWarps;
   if (DENSE) cudaMemsetAsync(buf->counters + 5, 0, sizeof(uint32_t), s);  // dense runs without tw_select
   launch_pdl(kern, dim3(grid), dim3(kAttThreads), smem, s, *kv, q, *buf, out, chunk, max_chunks, total);
-  launch_pdl(merge_kernel<G, DENSE>, dim3(units), dim3(256), 0, s, *kv, *buf, out, chunk, max_chunks);
+  launch_pdl(merge_kernel<G, DENSE>, dim3(units * G), dim3(kHeadDim), 0, s, *kv, *buf, out, chunk, max_chunks);
   return launch_status();
 }
 
