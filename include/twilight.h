@@ -101,6 +101,8 @@ typedef struct tw_decode_buffers {
   float* partials;          /* [max_items][G][d+2] split-KV partial (o[d], m, l) */
   uint32_t* head_page_bits; /* optional [Hq][ceil(max_pages/32)] per-head Quest page sets */
   uint32_t* sel_bits;       /* [U][T/32]         group-union bitmap over candidate positions */
+  int32_t* topp_done;       /* [U]               small-batch top-p: heads finished per unit (zero-initialised;
+                                                   left zeroed; with it, sel_bits must start zeroed too) */
   int32_t* band_idx;        /* [Hq][max_pages]   Quest pages in the fp32 filter's ambiguous band */
   double* band_scores;      /* [Hq][max_pages]   their exact fp64 bounds */
   int64_t max_items;

@@ -69,7 +69,7 @@ class TwDecodeBuffers(ctypes.Structure):
         ("head_stats", ctypes.c_void_p), ("final_idx", ctypes.c_void_p), ("final_count", ctypes.c_void_p),
         ("unit_items", ctypes.c_void_p), ("work_items", ctypes.c_void_p), ("counters", ctypes.c_void_p),
         ("partials", ctypes.c_void_p), ("head_page_bits", ctypes.c_void_p), ("sel_bits", ctypes.c_void_p),
-        ("band_idx", ctypes.c_void_p), ("band_scores", ctypes.c_void_p),
+        ("topp_done", ctypes.c_void_p), ("band_idx", ctypes.c_void_p), ("band_scores", ctypes.c_void_p),
         ("max_items", ctypes.c_int64),
     ]
 

@@ -644,6 +644,282 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
   }
 }
 
+// ---------------------------------------------------------------- small batches: one CTA per query head
+
+// When the batch has fewer (unit x head) pairs than SMs, one CTA per unit
+// leaves most SMs idle: here every query head gets its own CTA (pass 1, its
+// crossing, its pass 2 and resolve), the heads' kept positions are ORed into
+// the unit's bitmap in global memory, and the unit's last CTA compacts the
+// group union and leaves the bitmap and its counter zeroed.
+constexpr int kHeadThreads = 512;
+constexpr int kHeadMC = kMemberCap / 2;
+
+template <int G>
+__global__ void __launch_bounds__(kHeadThreads) topp_head_kernel(tw_paged_kv kv, tw_decode_params prm,
+                                                                 tw_decode_buffers buf) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int NT = kHeadThreads, NW = NT / 32, kPerT = kBins / NT;
+  extern __shared__ __align__(16) unsigned char sm[];
+  uint32_t* Hc = reinterpret_cast<uint32_t*>(sm);
+  uint32_t* Hu = Hc + kBins;
+  ResGroupSmem& S = *reinterpret_cast<ResGroupSmem*>(sm);  // aliases the bins once the crossing is known
+  uint32_t* mkey = reinterpret_cast<uint32_t*>(sm + (size_t)kBins * 8);
+  uint32_t* mpos = mkey + kHeadMC;
+  __shared__ HeadRec R;
+  __shared__ unsigned long long s_deep;
+  __shared__ int s_fill, s_last, s_first, s_bin;
+  __shared__ double s_dtmp[NW], s_above;
+  __shared__ uint32_t s_utmp[NW], s_acnt, s_wtot[NW];
+  const int unit = blockIdx.x / G, g = blockIdx.x % G, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Group grp = whole_block();
+  const size_t T = (size_t)kv.max_pages * kPage;
+  const size_t qh = (size_t)unit * G + g;
+  const int npos = buf.cand_count[unit] * kPage;
+  const int n4 = npos >> 2;
+  const float* z = buf.logits + qh * T;
+  uint32_t* ubits = buf.sel_bits + (size_t)unit * (T / 32);
+  const double p_eff = fmin(prm.p, 1.0) - 1e-9;
+  const float M = key2f(buf.head_max[qh]);
+  const bool empty = p_eff <= 0.0 || npos == 0 || !(M > -INFINITY);
+  if (tid == 0) {
+    HeadRec r{};
+    r.M = M;
+    r.cb = empty ? -2 : 0;
+    r.zhi = r.zlo = INFINITY;
+    r.seg = -1;
+    R = r;
+    s_fill = 0;
+    s_deep = 0;
+  }
+  if (!empty) {
+    for (int i = tid; i < kBins; i += NT) Hc[i] = Hu[i] = 0;
+    __syncthreads();
+    const float M120 = M * kBinPerLogit;
+    unsigned long long deep = 0;
+    for (int i = tid; i < n4; i += NT) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(z) + i);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float x = comp(v, e);
+        if (x > -INFINITY) {
+          const int b = dbin(x, M120);
+          const uint32_t d = deficit(x, M, b);
+          atomicAdd(&Hc[b], 1u);
+          if (b < kBins - 1) atomicAdd(&Hu[b], d);
+          else deep += d;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) deep += __shfl_xor_sync(0xffffffffu, deep, o);
+    if (lane == 0 && deep) atomicAdd(&s_deep, deep);
+    __syncthreads();
+    const int bfirst = tid * kPerT;
+    const float t0 = bin_top(M, bfirst);
+    const float w0 = (float)exp((double)t0 - (double)M);
+    auto mass = [&](int i, uint32_t& c) -> double {
+      const int bb = bfirst + i;
+      c = Hc[bb];
+      if (!c) return 0.0;
+      const uint64_t us = bb == kBins - 1 ? (uint64_t)s_deep : (uint64_t)Hu[bb];
+      const float d = (bin_top(M, bb) - t0) + (float)i * (1.0f / 120.0f);
+      const float w = w0 * kStepExpF[i] * (1.0f + d);
+      return (double)(w * ((float)c - (float)us * (float)kInvUscale));
+    };
+    double local = 0.0;
+    uint32_t lc = 0;
+#pragma unroll
+    for (int i = 0; i < kPerT; ++i) {
+      uint32_t c;
+      local += mass(i, c);
+      lc += c;
+    }
+    double Z;
+    uint32_t b0;
+    const double incl = grp_scan<double>(grp, local, s_dtmp, Z);
+    const uint32_t cincl = grp_scan<uint32_t>(grp, lc, s_utmp, b0);
+    const double target = p_eff * Z;
+    if (tid == 0) s_bin = -1;
+    __syncthreads();
+    const double excl = incl - local;
+    if (excl < target && target <= incl) {
+      double run = excl;
+      uint32_t crun = cincl - lc;
+#pragma unroll 1
+      for (int i = 0; i < kPerT; ++i) {
+        uint32_t c;
+        const double m = mass(i, c);
+        if (c && run + m >= target) {
+          s_bin = bfirst + i;
+          s_above = run;
+          s_acnt = crun;
+          break;
+        }
+        run += m;
+        crun += c;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int cb = s_bin;
+      R.cb = cb;
+      R.Z = Z;
+      R.target = target;
+      R.b0 = b0;
+      if (cb >= 0) {
+        R.above_mass = s_above;
+        R.above_cnt = s_acnt;
+        R.members = Hc[cb];
+        R.wb = exp((double)bin_top(M, cb) - (double)M);
+        R.zhi = bin_ceiling(cb, M, M120);
+        R.zlo = bin_ceiling(cb + 1, M, M120);
+        if (R.members <= (uint32_t)kHeadMC) R.seg = 0;
+        else R.zlo = R.zhi;  // members re-read from the logits
+      } else {
+        R.zhi = R.zlo = -INFINITY;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- pass 2 (this head): kept positions ORed into the unit bitmap, crossing-bin members listed
+  {
+    const float zhi = R.zhi, zlo = R.zlo;
+    for (int i0 = 0; i0 < n4; i0 += NT) {
+      const int i = i0 + tid;
+      const bool valid = i < n4;
+      const float4 v = valid ? __ldcg(reinterpret_cast<const float4*>(z) + i) : ninf4();
+      uint32_t nib = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float x = comp(v, e);
+        nib |= (x > zhi ? 1u : 0u) << e;
+        if (x > zlo && x <= zhi) {
+          const int sl = atomicAdd(&s_fill, 1);
+          mkey[sl] = f2key(x);
+          mpos[sl] = (uint32_t)(4 * i + e);
+        }
+      }
+      uint32_t w = nib << (4 * (lane & 7));
+      w |= __shfl_xor_sync(0xffffffffu, w, 1);
+      w |= __shfl_xor_sync(0xffffffffu, w, 2);
+      w |= __shfl_xor_sync(0xffffffffu, w, 4);
+      if ((lane & 7) == 0 && valid && w) atomicOr(ubits + (i >> 3), w);
+    }
+  }
+  __syncthreads();
+  // ---- resolve the threshold class of this head
+  {
+    const HeadRec& h = R;
+    uint32_t thr, sel_cnt = 0;
+    double sel_mass = 0.0;
+    if (h.cb == -2) {
+      thr = 0xFFFFFFFFu;
+    } else if (h.cb == -1) {
+      thr = 0u;
+      sel_cnt = h.b0;
+      sel_mass = h.Z;
+    } else {
+      uint32_t c = 0;
+      unsigned long long us = 0;
+      auto pick = [&](uint32_t k, uint32_t u, uint32_t pos) {
+        if (k >= thr) {
+          ++c;
+          us += u;
+          atomicOr(ubits + (pos >> 5), 1u << (pos & 31));
+        }
+      };
+      if (h.seg >= 0) {
+        const SmemSrc src{mkey, mpos, (int)h.members, h.M, h.cb};
+        thr = resolve_threshold(grp, src, h.above_mass, h.target, h.wb, S);
+        src.each(grp, pick);
+      } else {
+        const LogitSrc src{z, npos, h.M, h.cb};
+        thr = resolve_threshold(grp, src, h.above_mass, h.target, h.wb, S);
+        src.each(grp, pick);
+      }
+      uint32_t ct;
+      grp_scan<uint32_t>(grp, c, S.utmp, ct);
+      unsigned long long ut;
+      grp_scan<unsigned long long>(grp, us, S.ltmp, ut);
+      sel_cnt = h.above_cnt + ct;
+      sel_mass = h.above_mass + class_mass(h.wb, ct, ut);
+    }
+    if (tid == 0) {
+      float* stats = buf.head_stats + qh * 4;
+      const bool emp = h.cb == -2;
+      buf.head_thr[qh] = thr;
+      stats[0] = (float)sel_cnt;
+      stats[1] = emp ? 0.f : (float)(sel_mass / h.Z);
+      stats[2] = emp || thr == 0u ? 0.f : (float)(exp((double)key2f(thr) - (double)h.M) / h.Z);
+      stats[3] = (float)h.b0;
+    }
+  }
+  // ---- the unit's last head CTA compacts the union
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(buf.topp_done + unit, 1) == G - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int* cand = buf.cand_pages + (size_t)unit * kv.max_pages;
+  int* out = buf.final_idx + (size_t)unit * T;
+  const int words = (npos + 31) >> 5;
+  const int per_w = (words + NW - 1) / NW;
+  const int wlo = min(words, warp * per_w), whi = min(words, wlo + per_w);
+  uint32_t cnt = 0;
+  for (int w = wlo + lane; w < whi; w += 32) cnt += __popc(__ldcg(ubits + w));
+  cnt = warp_sum(cnt);
+  if (lane == 0) s_wtot[warp] = cnt;
+  __syncthreads();
+  uint32_t run = 0, basei = 0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    run += i < warp ? s_wtot[i] : 0u;
+    basei += s_wtot[i];
+  }
+  for (int w0 = wlo; w0 < whi; w0 += 32) {
+    const int w = w0 + lane;
+    const uint32_t x = w < whi ? __ldcg(ubits + w) : 0u;
+    if (w < whi) ubits[w] = 0u;  // leave the bitmap zeroed for the next step
+    const int pa = 2 * w0 + lane < kv.max_pages ? cand[2 * w0 + lane] : 0;
+    const int pb = 2 * w0 + 32 + lane < kv.max_pages ? cand[2 * w0 + 32 + lane] : 0;
+    uint32_t incl = __popc(x);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t wbase = run + incl - __popc(x);
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t xw = __shfl_sync(0xffffffffu, x, j);
+      const uint32_t bw = __shfl_sync(0xffffffffu, wbase, j);
+      const int src = (2 * j + (lane >> 4)) & 31;
+      const int qa = __shfl_sync(0xffffffffu, pa, src), qb = __shfl_sync(0xffffffffu, pb, src);
+      if ((xw >> lane) & 1u)
+        out[bw + __popc(xw & ((1u << lane) - 1u))] = (j < 16 ? qa : qb) * kPage + (lane & 15);
+    }
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : TW_DEFAULT_CHUNK;
+  const int nitems = ((int)basei + chunk - 1) / chunk;
+  if (tid == 0) {
+    buf.final_count[unit] = (int)basei;
+    s_first = nitems ? (int)atomicAdd(&buf.counters[0], (uint32_t)nitems) : 0;
+    buf.unit_items[2 * unit] = s_first;
+    buf.unit_items[2 * unit + 1] = nitems;
+    buf.topp_done[unit] = 0;
+  }
+  __syncthreads();
+  for (int i = tid; i < nitems; i += NT) {
+    if (s_first + i < buf.max_items) {
+      buf.work_items[2 * (s_first + i)] = unit;
+      buf.work_items[2 * (s_first + i) + 1] = i * chunk;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- Algorithm 1, literally
 
 __device__ __forceinline__ double block_sum_d(double v, double* tmp) { return block_sum<double>(v, tmp); }
@@ -742,7 +1018,16 @@ static int launch_unit(const tw_paged_kv* kv, const tw_decode_params* prm, const
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (G >= 2 && kv->num_seqs * kv->num_kv_heads > sms) return launch_unit_hb<G, kHB / 2>(kv, prm, buf, stream);
+  const int units = kv->num_seqs * kv->num_kv_heads;
+  if (G >= 2 && units * G <= sms && buf->topp_done) {  // few (unit, head) pairs: one CTA per query head
+    const size_t smem = (size_t)kBins * 8 + (size_t)kHeadMC * 8;
+    if (cudaFuncSetAttribute(topp_head_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return TW_ERR_CUDA;
+    launch_pdl(topp_head_kernel<G>, dim3(units * G), dim3(kHeadThreads), smem, stream, *kv, *prm, *buf);
+    return launch_status();
+  }
+  if (G >= 2 && units > sms) return launch_unit_hb<G, kHB / 2>(kv, prm, buf, stream);
   return launch_unit_hb<G, kHB>(kv, prm, buf, stream);
 }
 

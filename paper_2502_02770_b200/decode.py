@@ -206,12 +206,13 @@ class DecodeBuffers:
         words = -(-cache.max_pages // 32)
         self.head_page_bits = torch.zeros(Hq, words, dtype=torch.int32, device=dev) if head_page_bits else None
         self.sel_bits = torch.zeros(U, T // 32, dtype=torch.int32, device=dev)
+        self.topp_done = torch.zeros(U, dtype=torch.int32, device=dev)  # the library leaves it (and sel_bits) zeroed
         self.band_idx = torch.empty(Hq, cache.max_pages, dtype=torch.int32, device=dev)
         self.band_scores = torch.empty(Hq, cache.max_pages, dtype=torch.float64, device=dev)
         s = L.TwDecodeBuffers()
         for name in ("page_scores", "cand_pages", "cand_count", "logits", "head_max", "head_thr", "head_stats",
                      "final_idx", "final_count", "unit_items", "work_items", "counters", "partials",
-                     "head_page_bits", "sel_bits", "band_idx", "band_scores"):
+                     "head_page_bits", "sel_bits", "topp_done", "band_idx", "band_scores"):
             setattr(s, name, L.ptr(getattr(self, name)))
         s.max_items = self.max_items
         self._struct = s
