@@ -53,7 +53,12 @@ typedef enum {
 } tw_status;
 
 typedef enum { TW_F32 = 0, TW_BF16 = 1 } tw_dtype;
-typedef enum { TW_SELECT_FULL = 0, TW_SELECT_QUEST = 1, TW_SELECT_SINK_WINDOW = 2 } tw_selector;
+typedef enum {
+  TW_SELECT_FULL = 0,
+  TW_SELECT_QUEST = 1,
+  TW_SELECT_SINK_WINDOW = 2,
+  TW_SELECT_CHANNEL_PRUNED = 3
+} tw_selector;
 
 typedef struct tw_paged_kv {
   int32_t num_seqs;       /* B */
@@ -81,6 +86,12 @@ typedef struct tw_decode_params {
   int32_t renormalize;  /* must be 1 on this path (PipelineConfig.renormalize_output, pipeline.py:58) */
   int32_t sink;         /* sink-window selector (select_sink_window, selectors.py:164-175): first tokens kept */
   int32_t window;       /* ... and last tokens kept; every token when sink + window >= n */
+  int32_t top_channels; /* channel-pruned selector (select_channel_pruned, selectors.py:146-161): channels kept
+                           (0 = d / 8, build_selector :205-207) */
+  int32_t budget_tokens;/* channel-pruned selector: B0 in tokens (resolve_budget) */
+  int32_t channels_fixed;/* channel-pruned selector: 0 = rank the channels by mean |K| and write them to
+                           chan_ids; 1 = use the top_channels ids already in chan_ids (the slice fixed
+                           once per context, selectors.py:203) */
 } tw_decode_params;
 
 /* Intermediate buffers of one decode step (all caller-allocated, sizes in
@@ -100,7 +111,9 @@ typedef struct tw_decode_buffers {
   uint32_t* counters;       /* [8]               device-side counters (zeroed by tw_select) */
   float* partials;          /* [max_items][G][d+2] split-KV partial (o[d], m, l) */
   uint32_t* head_page_bits; /* optional [Hq][ceil(max_pages/32)] per-head Quest page sets */
-  uint32_t* sel_bits;       /* [U][T/32]         group-union bitmap over candidate positions */
+  uint32_t* sel_bits;       /* [U][ceil(T/32)]   group-union bitmap over candidate positions */
+  uint32_t* tok_mask;       /* [U][ceil(T/32)]        channel-pruned selector: selected tokens (the estimate's mask) */
+  int32_t* chan_ids;        /* [U][128]          channel-pruned selector: the channel slice (ascending) */
   int32_t* topp_done;       /* [U]               small-batch top-p: heads finished per unit (zero-initialised;
                                                    left zeroed; with it, sel_bits must start zeroed too) */
   int32_t* band_idx;        /* [Hq][max_pages]   Quest pages in the fp32 filter's ambiguous band */

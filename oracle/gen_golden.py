@@ -267,6 +267,54 @@ def main() -> None:
     t = (np.arange(2 * 3 * 5, dtype=np.float32).reshape(2, 3, 5) - 7.25) / 3.0
     write_tensor(os.path.join(OUT, "ref_tensor.twlt"), t)
     np.save(os.path.join(OUT, "ref_tensor.npy"), t)
+
+    # ---------------------------------------------------------- channel-pruned selector (selectors.py:135-161)
+    ch = {}
+    rng_c = np.random.default_rng(20250311)
+    for i, (n, count, dt) in enumerate(((300, 16, "f32"), (1000, 5, "bf16"), (64, 128, "f32"), (40, 1, "f32"))):
+        K = (rng_c.standard_normal((n, 128)) * np.exp(rng_c.standard_normal(128))).astype(np.float32)
+        if i == 3:  # magnitude ties: equal columns -> lower channel wins
+            K[:, 7] = K[:, 3]
+            K[:, 90] = -K[:, 3] * 4
+            K[:, 91] = K[:, 90]
+        if dt == "bf16":
+            K = bf16_round(K)
+        ch[f"m{i}/K"], ch[f"m{i}/count"] = K, np.array([count])
+        ch[f"m{i}/ids"] = nk.selectors.top_channels_by_magnitude(K, count)
+    for i, (n, count, budget, dt) in enumerate(((500, 16, 77, "f32"), (333, 9, 0.3, "bf16"),
+                                                 (96, 3, 200, "f32"), (50, 16, 1, "bf16"))):
+        K = rng_c.standard_normal((n, 128)).astype(np.float32)
+        q = rng_c.standard_normal(128).astype(np.float32)
+        if dt == "bf16":
+            K, q = bf16_round(K), bf16_round(q)
+        if i == 2:  # score ties: repeated rows -> lower token first
+            K[50:60] = K[10]
+        ids = np.sort(rng_c.choice(128, size=count, replace=False))
+        sel = nk.selectors.select_channel_pruned(q, K[:, ids].astype(np.float64), ids, budget)
+        ch[f"s{i}/K"], ch[f"s{i}/q"], ch[f"s{i}/ids"] = K, q, ids
+        ch[f"s{i}/budget"] = np.array([budget, 1.0 if isinstance(budget, float) else 0.0])
+        ch[f"s{i}/indices"] = sel.indices
+    for i, (n, G, budget, top, p, tau, dt) in enumerate(((700, 4, 96, None, 0.9, 0.4, "bf16"),
+                                                         (512, 1, 0.25, 24, 0.95, 0.6, "f32"),
+                                                         (900, 2, 300, 8, 0.85, 1.0, "f32"))):
+        K = rng_c.standard_normal((n, 128)).astype(np.float32)
+        V = rng_c.standard_normal((n, 128)).astype(np.float32)
+        Q = (rng_c.standard_normal((G, 128)) / tau).astype(np.float32)
+        if dt == "bf16":
+            K, V, Q = bf16_round(K), bf16_round(V), bf16_round(Q)
+        sel = nk.SelectorConfig(kind="channel_pruned", budget=budget, page_size=16, top_channels=top)
+        cfg = nk.PipelineConfig(selector=sel, prune=nk.BinarySearchConfig(p=p), group_map=nk.GroupMap(G))
+        if G == 1:
+            out, outcome, report = nk.run_head(Q[0], K, V, cfg)
+            outs, finals, b0 = out[None], [outcome.selection.indices], [report.b0]
+        else:
+            outs, outcomes, reports = nk.run_grouped(Q, K, V, cfg)
+            finals, b0 = [o.selection.indices for o in outcomes], [r.b0 for r in reports]
+        ch[f"p{i}/K"], ch[f"p{i}/V"], ch[f"p{i}/Q"] = K, V, Q
+        # budget, p, budget-is-fraction, top_channels (-1: default d // 8)
+        ch[f"p{i}/cfg"] = np.array([budget, p, 1.0 if isinstance(budget, float) else 0.0, -1 if top is None else top])
+        ch[f"p{i}/out"], ch[f"p{i}/final"], ch[f"p{i}/b0"] = np.asarray(outs), finals[0], np.array(b0)
+    np.savez_compressed(os.path.join(OUT, "channel.npz"), **ch)
     print("golden vectors written to", OUT)
 
 

@@ -209,6 +209,30 @@ def sink_window_tokens(n: int, sink: int, window: int) -> np.ndarray:
     return np.unique(np.concatenate([np.arange(sink), np.arange(n - window, n)])).astype(np.int64)
 
 
+def top_channels_by_magnitude(K: np.ndarray, count: int) -> np.ndarray:
+    """selectors.py:135-143: the ``count`` channels of largest mean |K| (fp64;
+    NumPy's axis-0 mean adds the rows in order), stable on ties, ascending."""
+    K = np.asarray(K, dtype=np.float64)
+    if K.ndim != 2:
+        raise ValueError("keys must be (n, d)")
+    if not 1 <= count <= K.shape[1]:
+        raise ValueError(f"count {count} outside [1, {K.shape[1]}]")
+    magnitude = np.abs(K).mean(axis=0)
+    return np.sort(np.argsort(-magnitude, kind="stable")[:count])
+
+
+def channel_pruned_tokens(q, K, ids, budget) -> np.ndarray:
+    """select_channel_pruned (selectors.py:146-161): the B0 tokens with the
+    largest (K[:, ids] @ q[ids]) / sqrt(d) in fp64, ties -> lower token; sorted."""
+    q = np.asarray(q, dtype=np.float64)
+    ids = np.asarray(ids, dtype=np.int64)
+    Kr = np.asarray(K, dtype=np.float64)[:, ids]
+    n = Kr.shape[0]
+    b0 = resolve_budget(budget, n)
+    scores = (Kr @ q[ids]) / math.sqrt(q.size)
+    return np.sort(np.argsort(-scores, kind="stable")[:b0])
+
+
 def union_sorted(index_sets) -> np.ndarray:
     """Sorted union of index arrays (group_union, selectors.py:178-186)."""
     sets = [np.asarray(s, dtype=np.int64) for s in index_sets]
@@ -373,7 +397,7 @@ def prepare_unit(K, page_size: int = PAGE_SIZE, bits: int = 4):
 
 def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.95,
                 page_size: int = PAGE_SIZE, renormalize: bool = True, logits_override=None, prepared=None,
-                sink: int = 4, window: int = 64, bits: int = 4):
+                sink: int = 4, window: int = 64, bits: int = 4, top_channels=None):
     """run_grouped's hot path for one KV head (pipeline.py:306-360):
 
     per-head Quest (selectors.py:112-132; or select_full :90-94, or
@@ -383,8 +407,9 @@ def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.9
     search (:345) -> group set = union of the pruned sets (:347) -> every
     head attends to the group set with renormalised full-context weights
     (:366-375).  With G == 1 this is run_head (pipeline.py:286-303; equal
-    per test_pipeline.py:232-241).  ``selector`` is "quest", "full" or
-    "sink_window".
+    per test_pipeline.py:232-241).  ``selector`` is "quest", "full",
+    "sink_window" or "channel_pruned" (selectors.py:135-161, channel slice
+    fixed per context as build_selector :203-209 does; token sets, not pages).
 
     ``logits_override`` (G, |union|) replaces the INT4 estimate, so a test
     can feed the GPU's logits to the oracle's softmax + search;
@@ -399,12 +424,19 @@ def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.9
         head_pages = [np.arange(lo.shape[0]) for _ in range(G)]
     elif selector == "quest":
         head_pages = [quest_select_pages(Q[h], lo, hi, budget, n, page_size) for h in range(G)]
-    elif selector == "sink_window":
+    elif selector in ("sink_window", "channel_pruned"):
         head_pages = None
     else:
         raise ValueError(f"selector {selector!r} not on the accelerated path")
-    if head_pages is None:
+    head_tokens = None
+    if selector == "sink_window":
         cand = sink_window_tokens(n, sink, window)  # the same for every head: the union is the set itself
+        union_pages = np.unique(cand // page_size)
+    elif selector == "channel_pruned":
+        count = top_channels if top_channels is not None else max(1, K.shape[1] // 8)
+        ids = top_channels_by_magnitude(K, count)
+        head_tokens = [channel_pruned_tokens(Q[h], K, ids, budget) for h in range(G)]
+        cand = union_sorted(head_tokens)
         union_pages = np.unique(cand // page_size)
     else:
         union_pages = union_sorted(head_pages)
@@ -427,7 +459,7 @@ def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.9
         out[h] = subset_attention(w_full, V, shared, ok)
     return {
         "lo": lo, "hi": hi, "codes": codes, "scale": scale, "zero": zero,
-        "head_pages": head_pages, "union_pages": union_pages, "candidates": cand,
+        "head_pages": head_pages, "head_tokens": head_tokens, "union_pages": union_pages, "candidates": cand,
         "logits": logits, "pruned": pruned, "thresholds": thresholds, "iterations": iters,
         "final": shared, "out": out,
     }

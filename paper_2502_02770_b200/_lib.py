@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("TW_LIB_PATH") or os.path.join(HERE, "_lib", "libtwili
 
 TW_OK, TW_ERR_INVALID, TW_ERR_INDEX, TW_ERR_DEGENERATE, TW_ERR_CUDA = range(5)
 TW_F32, TW_BF16 = 0, 1
-TW_SELECT_FULL, TW_SELECT_QUEST, TW_SELECT_SINK_WINDOW = 0, 1, 2
+TW_SELECT_FULL, TW_SELECT_QUEST, TW_SELECT_SINK_WINDOW, TW_SELECT_CHANNEL_PRUNED = 0, 1, 2, 3
 PAGE_SIZE = 16
 DEFAULT_CHUNK = 512
 QBLOCK_BYTES = 1152
@@ -58,7 +58,8 @@ class TwDecodeParams(ctypes.Structure):
     _fields_ = [
         ("selector", ctypes.c_int32), ("budget_pages", ctypes.c_int32), ("p", ctypes.c_double),
         ("chunk_tokens", ctypes.c_int32), ("renormalize", ctypes.c_int32), ("sink", ctypes.c_int32),
-        ("window", ctypes.c_int32),
+        ("window", ctypes.c_int32), ("top_channels", ctypes.c_int32), ("budget_tokens", ctypes.c_int32),
+        ("channels_fixed", ctypes.c_int32),
     ]
 
 
@@ -69,7 +70,7 @@ class TwDecodeBuffers(ctypes.Structure):
         ("head_stats", ctypes.c_void_p), ("final_idx", ctypes.c_void_p), ("final_count", ctypes.c_void_p),
         ("unit_items", ctypes.c_void_p), ("work_items", ctypes.c_void_p), ("counters", ctypes.c_void_p),
         ("partials", ctypes.c_void_p), ("head_page_bits", ctypes.c_void_p), ("sel_bits", ctypes.c_void_p),
-        ("topp_done", ctypes.c_void_p), ("band_idx", ctypes.c_void_p), ("band_scores", ctypes.c_void_p),
+        ("tok_mask", ctypes.c_void_p), ("chan_ids", ctypes.c_void_p), ("topp_done", ctypes.c_void_p), ("band_idx", ctypes.c_void_p), ("band_scores", ctypes.c_void_p),
         ("max_items", ctypes.c_int64),
     ]
 

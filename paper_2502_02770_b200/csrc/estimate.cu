@@ -191,7 +191,8 @@ __device__ __forceinline__ void estimate_prologue_packed(const T* __restrict__ q
 template <typename T, int G, int BITS>
 __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv, const T* __restrict__ q,
                                                                   tw_decode_buffers buf, int max_chunks,
-                                                                  int sw_sink, int sw_window) {
+                                                                  int sw_sink, int sw_window,
+                                                                  const uint32_t* __restrict__ tok_mask) {
   pdl_wait();
   pdl_trigger();
   constexpr int kBlock = qblock_bytes_for(BITS), kCodes = code_bytes_for(BITS), kRowBytes = kHeadDim * BITS / 8;
@@ -340,8 +341,13 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       const int tok_r = lp * kPage + r;
       // sink-window selection (selectors.py:164-175): tokens between the sink and the window are not candidates
       const bool swm = sw_window >= 0 && sw_sink + sw_window < n;
-      const bool v_r = tok_r < n && (!swm || tok_r < sw_sink || tok_r >= n - sw_window);
-      const bool v_r8 = tok_r + 8 < n && (!swm || tok_r + 8 < sw_sink || tok_r + 8 >= n - sw_window);
+      bool v_r = tok_r < n && (!swm || tok_r < sw_sink || tok_r >= n - sw_window);
+      bool v_r8 = tok_r + 8 < n && (!swm || tok_r + 8 < sw_sink || tok_r + 8 >= n - sw_window);
+      if (tok_mask) {  // channel-pruned selection: only the selected tokens of a candidate page
+        const uint32_t mw = __ldg(tok_mask + (size_t)unit * ((T_stride + 31) / 32) + (tok_r >> 5));
+        v_r = v_r && ((mw >> (tok_r & 31)) & 1u);
+        v_r8 = v_r8 && ((mw >> ((tok_r + 8) & 31)) & 1u);
+      }
       const int ci = c0 + i;
       if constexpr (kPacked) {
         if (t < G) {
@@ -415,7 +421,7 @@ using namespace tw;
 
 template <typename T, int G, int BITS>
 static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, int sw_sink,
-                              int sw_window, cudaStream_t stream) {
+                              int sw_window, const uint32_t* tok_mask, cudaStream_t stream) {
   const int max_chunks = (kv->max_pages + kEstPagesPerCta - 1) / kEstPagesPerCta;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
@@ -425,18 +431,18 @@ static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode
   int grid = sms * persist_cap(per_sm);
   if (grid * kEstWarps > items) grid = (items + kEstWarps - 1) / kEstWarps;
   launch_pdl(estimate_kernel<T, G, BITS>, dim3(grid), dim3(kEstWarps * 32), 0, stream, *kv, q, *buf, max_chunks, sw_sink,
-             sw_window);
+             sw_window, tok_mask);
 }
 
 template <typename T>
 static int launch_estimate(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, int ss, int sw,
-                           cudaStream_t stream) {
+                           const uint32_t* tm, cudaStream_t stream) {
   auto by_bits = [&](auto gtag) {
     constexpr int GG = decltype(gtag)::value;
     switch (cache_bits(*kv)) {
-      case 2: launch_estimate_g<T, GG, 2>(kv, q, buf, ss, sw, stream); break;
-      case 8: launch_estimate_g<T, GG, 8>(kv, q, buf, ss, sw, stream); break;
-      default: launch_estimate_g<T, GG, 4>(kv, q, buf, ss, sw, stream); break;
+      case 2: launch_estimate_g<T, GG, 2>(kv, q, buf, ss, sw, tm, stream); break;
+      case 8: launch_estimate_g<T, GG, 8>(kv, q, buf, ss, sw, tm, stream); break;
+      default: launch_estimate_g<T, GG, 4>(kv, q, buf, ss, sw, tm, stream); break;
     }
   };
   switch (kv->group_size) {
@@ -454,9 +460,11 @@ extern "C" int tw_estimate(const tw_paged_kv* kv, const void* q, const tw_decode
   if (!kv || !q || !buf || kv->head_dim != kHeadDim || !buf->logits || !buf->head_max) return TW_ERR_INVALID;
   const bool sw = prm && prm->selector == TW_SELECT_SINK_WINDOW;
   const int ss = sw ? prm->sink : 0, swin = sw ? prm->window : -1;
+  const uint32_t* tm = prm && prm->selector == TW_SELECT_CHANNEL_PRUNED ? buf->tok_mask : nullptr;
+  if (prm && prm->selector == TW_SELECT_CHANNEL_PRUNED && !tm) return TW_ERR_INVALID;
   // head_max is zeroed by tw_select (quest_select_kernel), which always precedes this call
-  if (kv->dtype == TW_BF16) return launch_estimate<__nv_bfloat16>(kv, (const __nv_bfloat16*)q, buf, ss, swin, stream);
-  return launch_estimate<float>(kv, (const float*)q, buf, ss, swin, stream);
+  if (kv->dtype == TW_BF16) return launch_estimate<__nv_bfloat16>(kv, (const __nv_bfloat16*)q, buf, ss, swin, tm, stream);
+  return launch_estimate<float>(kv, (const float*)q, buf, ss, swin, tm, stream);
 }
 
 extern "C" int tw_estimate_tokens(const tw_paged_kv* kv, int32_t seq, int32_t kv_head, const void* q,

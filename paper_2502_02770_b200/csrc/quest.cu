@@ -557,8 +557,12 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
   return launch_status();
 }
 
+int tw_select_channel_pruned(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
+                             const tw_decode_buffers* buf, cudaStream_t stream);  // channel.cu
+
 extern "C" int tw_select(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
                          const tw_decode_buffers* buf, cudaStream_t stream) {
+  if (prm && prm->selector == TW_SELECT_CHANNEL_PRUNED) return tw_select_channel_pruned(kv, q, prm, buf, stream);
   if (!kv || !prm || !buf || kv->head_dim != kHeadDim || !buf->cand_pages || !buf->cand_count || !buf->counters ||
       !buf->head_max)
     return TW_ERR_INVALID;

@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
   const int npos = buf.cand_count[unit] * kPage;
   const int n4 = npos >> 2;
   const float* zu = buf.logits + (size_t)unit * G * T;
-  uint32_t* ubits = buf.sel_bits + (size_t)unit * (T / 32);
+  uint32_t* ubits = buf.sel_bits + (size_t)unit * ((T + 31) / 32);
   const double p_eff = fmin(prm.p, 1.0) - 1e-9;
   if (tid < G) {
     const float M = key2f(buf.head_max[(size_t)unit * G + tid]);  // NaN when the head has no valid logit
@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(kHeadThreads) topp_head_kernel(tw_paged_kv kv,
   const int npos = buf.cand_count[unit] * kPage;
   const int n4 = npos >> 2;
   const float* z = buf.logits + qh * T;
-  uint32_t* ubits = buf.sel_bits + (size_t)unit * (T / 32);
+  uint32_t* ubits = buf.sel_bits + (size_t)unit * ((T + 31) / 32);
   const double p_eff = fmin(prm.p, 1.0) - 1e-9;
   const float M = key2f(buf.head_max[qh]);
   const bool empty = p_eff <= 0.0 || npos == 0 || !(M > -INFINITY);

@@ -205,14 +205,16 @@ class DecodeBuffers:
         self.partials = torch.empty(self.max_items, G, L.HEAD_DIM + 2, dtype=torch.float32, device=dev)
         words = -(-cache.max_pages // 32)
         self.head_page_bits = torch.zeros(Hq, words, dtype=torch.int32, device=dev) if head_page_bits else None
-        self.sel_bits = torch.zeros(U, T // 32, dtype=torch.int32, device=dev)
+        self.sel_bits = torch.zeros(U, -(-T // 32), dtype=torch.int32, device=dev)
         self.topp_done = torch.zeros(U, dtype=torch.int32, device=dev)  # the library leaves it (and sel_bits) zeroed
+        self.tok_mask = torch.zeros(U, -(-T // 32), dtype=torch.int32, device=dev)  # channel-pruned selections
+        self.chan_ids = torch.zeros(U, L.HEAD_DIM, dtype=torch.int32, device=dev)  # channel-pruned slice
         self.band_idx = torch.empty(Hq, cache.max_pages, dtype=torch.int32, device=dev)
         self.band_scores = torch.empty(Hq, cache.max_pages, dtype=torch.float64, device=dev)
         s = L.TwDecodeBuffers()
         for name in ("page_scores", "cand_pages", "cand_count", "logits", "head_max", "head_thr", "head_stats",
                      "final_idx", "final_count", "unit_items", "work_items", "counters", "partials",
-                     "head_page_bits", "sel_bits", "topp_done", "band_idx", "band_scores"):
+                     "head_page_bits", "sel_bits", "tok_mask", "chan_ids", "topp_done", "band_idx", "band_scores"):
             setattr(s, name, L.ptr(getattr(self, name)))
         s.max_items = self.max_items
         self._struct = s
@@ -231,12 +233,19 @@ class TwilightDecoder:
     """Runs the select -> estimate -> prune -> attend path for one layer.
 
     selector: "quest" (Quest page top-k with budget B0 tokens), "full", or
-    "sink_window" (the first ``sink`` + last ``window`` tokens, selectors.py:164-175).
+    "sink_window" (the first ``sink`` + last ``window`` tokens, selectors.py:164-175), or
+    "channel_pruned" (per query head the ``budget`` tokens with the largest
+    partial logit over the ``top_channels`` channels of largest mean |K|,
+    selectors.py:135-161; contexts up to 32768 tokens).  With
+    ``fix_channels`` the channel slice ranked at the first step is kept for the
+    following steps (the reference binds it once per context, selectors.py:203);
+    otherwise it is re-ranked over the current cache every step.
     """
 
     def __init__(self, cache: PagedKVCache, selector: str = "quest", budget=None, p: float = 0.95,
                  chunk_tokens: int | None = None, head_page_bits: bool = False,
-                 bufs: DecodeBuffers | list | None = None, waves: int = 1, sink: int = 4, window: int = 64):
+                 bufs: DecodeBuffers | list | None = None, waves: int = 1, sink: int = 4, window: int = 64,
+                 top_channels: int | None = None, fix_channels: bool = False):
         self.waves = []
         if waves > 1:
             # sub-batches on their own streams: the select/top-p stages of one wave
@@ -247,15 +256,19 @@ class TwilightDecoder:
             for w in range(waves):
                 sub = TwilightDecoder(cache.view(w * per, (w + 1) * per), selector, budget, p, chunk_tokens,
                                       head_page_bits, bufs[w] if isinstance(bufs, list) else None,
-                                      sink=sink, window=window)
+                                      sink=sink, window=window, top_channels=top_channels,
+                                      fix_channels=fix_channels)
                 self.waves.append((w * per, (w + 1) * per, sub, torch.cuda.Stream(device=cache.device)))
             self.cache = cache
             self.params = self.waves[0][2].params
             self.bufs = [wv[2].bufs for wv in self.waves]
             return
         chunk_tokens = chunk_tokens or auto_chunk(cache)
-        if selector not in ("quest", "full", "sink_window"):
-            raise ValueError(f"selector {selector!r} is not on the accelerated path (quest | full | sink_window)")
+        if selector not in ("quest", "full", "sink_window", "channel_pruned"):
+            raise ValueError(f"selector {selector!r} is not on the accelerated path "
+                             "(quest | full | sink_window | channel_pruned)")
+        if top_channels is not None and not 1 <= int(top_channels) <= L.HEAD_DIM:
+            raise ValueError(f"top_channels {top_channels} outside [1, {L.HEAD_DIM}]")
         if selector == "sink_window" and (sink < 0 or window < 0 or sink + window < 1):
             raise ValueError("sink and window must be non-negative and keep at least one token")
         if not 0.0 <= p <= 1.0:
@@ -264,9 +277,14 @@ class TwilightDecoder:
         # buffers may be shared by decoders of layers with the same geometry
         self.bufs = bufs if bufs is not None else DecodeBuffers(cache, chunk_tokens, head_page_bits)
         self.params = L.TwDecodeParams()
+        self.selector_name = selector
         self.params.selector = {"quest": L.TW_SELECT_QUEST, "full": L.TW_SELECT_FULL,
-                                "sink_window": L.TW_SELECT_SINK_WINDOW}[selector]
+                                "sink_window": L.TW_SELECT_SINK_WINDOW,
+                                "channel_pruned": L.TW_SELECT_CHANNEL_PRUNED}[selector]
         self.params.sink, self.params.window = int(sink), int(window)
+        # build_selector (selectors.py:205-207): d // 8 channels unless given
+        self.params.top_channels = int(top_channels) if top_channels is not None else max(1, L.HEAD_DIM // 8)
+        self.fix_channels = bool(fix_channels)
         self.params.p = float(p)
         self.params.chunk_tokens = chunk_tokens
         self.params.renormalize = 1
@@ -277,7 +295,14 @@ class TwilightDecoder:
             self.params.budget_pages = self.cache.max_pages
             return
         if budget is None:
-            raise ValueError("selector 'quest' requires a budget")
+            raise ValueError(f"selector {self.selector_name!r} requires a budget")
+        if self.params.selector == L.TW_SELECT_CHANNEL_PRUNED:
+            from .selectors import resolve_budget
+            if isinstance(budget, float) and n is None:
+                raise ValueError("a fractional budget needs the context length n")
+            self.params.budget_tokens = resolve_budget(budget, n if n is not None else int(budget))
+            self.params.budget_pages = self.cache.max_pages
+            return
         if isinstance(budget, float):
             if n is None:
                 raise ValueError("a fractional budget needs the context length n")
@@ -292,6 +317,8 @@ class TwilightDecoder:
     def select(self, q: torch.Tensor) -> None:
         kv, prm, buf = self._args()
         L.check(L.lib().tw_select(kv, L.ptr(q), prm, buf, L.stream_handle()), "tw_select")
+        if self.fix_channels and self.params.selector == L.TW_SELECT_CHANNEL_PRUNED:
+            self.params.channels_fixed = 1
 
     def estimate(self, q: torch.Tensor) -> None:
         kv, prm, buf = self._args()

@@ -116,7 +116,7 @@ def _spearman(a: torch.Tensor, b: torch.Tensor) -> float:
 
 
 def _check_cfg(cfg: PipelineConfig) -> None:
-    if cfg.selector.kind not in ("full", "quest", "sink_window"):
+    if cfg.selector.kind not in ("full", "quest", "sink_window", "channel_pruned"):
         raise NotImplementedError(f"selector {cfg.selector.kind!r} is not on the B200 path")
     if cfg.estimator_bits not in (2, 4, 8):
         raise NotImplementedError("the B200 path estimates with a 2-, 4- or 8-bit cache (estimator_bits)")
@@ -145,6 +145,11 @@ def _run(Q: torch.Tensor, keys: torch.Tensor, values: torch.Tensor, cfg: Pipelin
         dec = TwilightDecoder(kv, "quest", budget=resolve_budget(cfg.selector.budget, n), p=cfg.prune.p)
     elif cfg.selector.kind == "sink_window":
         dec = TwilightDecoder(kv, "sink_window", p=cfg.prune.p, sink=cfg.selector.sink, window=cfg.selector.window)
+    elif cfg.selector.kind == "channel_pruned":
+        if cfg.selector.budget is None:
+            raise ValueError("selector 'channel_pruned' requires a budget")
+        dec = TwilightDecoder(kv, "channel_pruned", budget=resolve_budget(cfg.selector.budget, n), p=cfg.prune.p,
+                              top_channels=cfg.selector.top_channels)
     else:
         dec = TwilightDecoder(kv, "full", p=cfg.prune.p)
     q = Q.to(dt).reshape(groups, G, L.HEAD_DIM).contiguous()

@@ -3,8 +3,9 @@
 ``quest_page_scores``, ``select_quest`` and ``group_union`` run on the B200
 kernels (tw_quest_scores / tw_select); ``select_full``, ``select_sink_window``
 and ``resolve_budget`` are index arithmetic (the decode path runs sink-window
-selection inside tw_select / tw_estimate).  The channel-pruned selector is not
-on the accelerated path and raises NotImplementedError.
+selection inside tw_select / tw_estimate).  ``top_channels_by_magnitude`` and
+``select_channel_pruned`` run on the channel-pruned selector kernel
+(csrc/channel.cu, tw_select with TW_SELECT_CHANNEL_PRUNED).
 """
 
 from __future__ import annotations
@@ -127,8 +128,80 @@ def group_union(selections) -> TokenSelection:
     return TokenSelection.from_indices(merged, n)
 
 
-def select_channel_pruned(*args, **kwargs):
-    raise NotImplementedError("channel-pruned selection is not on the B200 path (SURVEY.md 2.1)")
+def _channel_unit(keys_full: torch.Tensor):
+    """A one-unit cache holding ``keys_full`` [n, 128]."""
+    from .decode import PagedKVCache, pages_for
+    n = int(keys_full.shape[0])
+    if n < 1:
+        raise ValueError("context must contain at least one token")
+    cache = PagedKVCache(1, 1, 1, max_pages=pages_for(n), dtype=keys_full.dtype, device=keys_full.device)
+    cache.prefill(keys_full[None, None], torch.zeros_like(keys_full)[None, None])
+    return cache
+
+
+def _run_channel_select(cache, q, count: int, b0: int, ids=None):
+    from .decode import TwilightDecoder
+    dec = TwilightDecoder(cache, "channel_pruned", budget=b0, p=1.0, top_channels=count)
+    if ids is not None:
+        dec.bufs.chan_ids[0, :count] = ids.to(torch.int32)
+        dec.params.channels_fixed = 1
+    qv = torch.as_tensor(q, device=cache.device).to(cache.dtype).reshape(1, 1, L.HEAD_DIM).contiguous()
+    dec.select(qv)
+    return dec
+
+
+def top_channels_by_magnitude(keys, count: int) -> torch.Tensor:
+    """selectors.py:135-143: the ``count`` channels with the largest mean |K|
+    (fp64, rows summed in token order; ties -> lower channel), ascending.  Runs
+    the magnitude pass of the channel-pruned selector kernel."""
+    K = torch.as_tensor(keys)
+    if K.ndim != 2:
+        raise ValueError("keys must be (n, d)")
+    if not 1 <= count <= K.shape[1]:
+        raise ValueError(f"count {count} outside [1, {K.shape[1]}]")
+    if K.shape[1] != L.HEAD_DIM:
+        raise ValueError(f"the B200 path is compiled for d = {L.HEAD_DIM}")
+    if not K.is_cuda:
+        raise ValueError("keys must be a CUDA tensor (the Twilight path has no CPU fallback)")
+    K = K if K.dtype in (torch.bfloat16, torch.float32) else K.float()
+    cache = _channel_unit(K.contiguous())
+    dec = _run_channel_select(cache, torch.zeros(L.HEAD_DIM, device=K.device), count, 1)
+    return dec.bufs.chan_ids[0, :count].long()
+
+
+def select_channel_pruned(q, keys_reduced, channel_ids, budget) -> TokenSelection:
+    """selectors.py:146-161: the B0 tokens with the largest approximate logit
+    (K[:, ids] @ q[ids]) / sqrt(d), ties -> lower token, sorted.  Tokens whose
+    fp64 scores differ only in the last bits may be ordered differently from the
+    reference's BLAS reduction order (the kernel adds in ``channel_ids`` order)."""
+    qv = torch.as_tensor(q)
+    Kr = torch.as_tensor(keys_reduced)
+    ids = torch.as_tensor(channel_ids).long().reshape(-1)
+    if Kr.ndim != 2 or Kr.shape[1] != ids.numel():
+        raise ValueError("keys_reduced must be (n, len(channel_ids))")
+    if ids.numel() == 0 or bool((ids < 0).any()) or bool((ids >= qv.numel()).any()):
+        raise ValueError("channel ids outside the query dimension")
+    if qv.numel() != L.HEAD_DIM:
+        raise ValueError(f"the B200 path is compiled for d = {L.HEAD_DIM}")
+    if torch.unique(ids).numel() != ids.numel():
+        raise ValueError("repeated channel ids are not supported on the B200 path")
+    if not Kr.is_cuda:
+        raise ValueError("keys must be a CUDA tensor (the Twilight path has no CPU fallback)")
+    n = int(Kr.shape[0])
+    b0 = resolve_budget(budget, n)
+    dt = Kr.dtype if Kr.dtype in (torch.bfloat16, torch.float32) else torch.float32
+    full = torch.zeros(n, L.HEAD_DIM, dtype=dt, device=Kr.device)
+    full[:, ids.to(Kr.device)] = Kr.to(dt)
+    dec = _run_channel_select(_channel_unit(full), qv.to(Kr.device), ids.numel(), b0, ids.to(Kr.device))
+    return TokenSelection.from_indices(channel_selection(dec, 0, n), n)
+
+
+def channel_selection(dec, unit: int, n: int) -> torch.Tensor:
+    """Token indices of a unit's channel-pruned selection (tok_mask), ascending."""
+    words = dec.bufs.tok_mask[unit, : -(-n // 32)].long() & 0xFFFFFFFF
+    bits = (words[:, None] >> torch.arange(32, device=words.device)) & 1
+    idx = torch.nonzero(bits.reshape(-1)).reshape(-1)
+    return idx[idx < n]
 
 
 def select_sink_window(n: int, sink: int, window: int, device="cuda") -> TokenSelection:
@@ -146,22 +219,22 @@ def select_sink_window(n: int, sink: int, window: int, device="cuda") -> TokenSe
     return TokenSelection.from_indices(idx, n)
 
 
-def top_channels_by_magnitude(*args, **kwargs):
-    raise NotImplementedError("channel-pruned selection is not on the B200 path (SURVEY.md 2.1)")
-
-
 def build_selector(cfg: SelectorConfig, keys, metadata=None) -> Callable:
-    """selectors.py:189-209 for the accelerated kinds (full, quest, sink_window)."""
+    """selectors.py:189-209."""
     n = int(keys.shape[0])
     dev = keys.device if isinstance(keys, torch.Tensor) else "cuda"
     if cfg.kind == "full":
         return lambda q: select_full(n, dev)
     if cfg.kind == "sink_window":
         return lambda q: select_sink_window(n, cfg.sink, cfg.window, dev)
-    if cfg.kind == "channel_pruned":
-        raise NotImplementedError(f"selector {cfg.kind!r} is not on the B200 path")
     if cfg.budget is None:
         raise ValueError(f"selector {cfg.kind!r} requires a budget")
+    if cfg.kind == "channel_pruned":  # the channel slice is fixed once per context
+        K = torch.as_tensor(keys)
+        count = cfg.top_channels if cfg.top_channels is not None else max(1, K.shape[1] // 8)
+        ids = top_channels_by_magnitude(K, count)
+        reduced = K[:, ids]
+        return lambda q: select_channel_pruned(q, reduced, ids, cfg.budget)
     if metadata is None:
         raise ValueError("quest selector requires page metadata")
     return lambda q: select_quest(q, metadata, cfg.budget, cfg.page_size, n)

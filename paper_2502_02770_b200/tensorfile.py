@@ -129,6 +129,11 @@ def run_file_workload(path, cfg, dtype=torch.bfloat16, device="cuda"):
         dec = TwilightDecoder(cache, "quest", budget=resolve_budget(sel.budget, n), p=cfg.prune.p)
     elif sel.kind == "sink_window":
         dec = TwilightDecoder(cache, "sink_window", p=cfg.prune.p, sink=sel.sink, window=sel.window)
+    elif sel.kind == "channel_pruned":
+        if sel.budget is None:
+            raise ValueError("selector 'channel_pruned' requires a budget")
+        dec = TwilightDecoder(cache, "channel_pruned", budget=resolve_budget(sel.budget, n), p=cfg.prune.p,
+                              top_channels=sel.top_channels)
     else:
         dec = TwilightDecoder(cache, "full", p=cfg.prune.p)
     qd = torch.from_numpy(q).to(device=device, dtype=dtype)

@@ -269,3 +269,49 @@ def test_run_grouped_with_two_and_eight_bit_estimators(bits):
         np.testing.assert_allclose(out.cpu().numpy(), res["out"], rtol=2e-2, atol=2e-2 * np.abs(res["out"]).max())
     else:
         assert np.setxor1d(final, res["final"]).size <= 2  # threshold ties only
+
+
+def test_channel_pruned_api_matches_reference(golden):
+    """top_channels_by_magnitude / select_channel_pruned / run_grouped with the
+    channel-pruned selector against the reference's own outputs."""
+    for name, c in golden("channel").items():
+        if name.startswith("m"):
+            got = tw.top_channels_by_magnitude(as_input(c["K"]), int(c["count"][0]))
+            np.testing.assert_array_equal(got.cpu().numpy(), c["ids"], err_msg=name)
+        elif name.startswith("s"):
+            budget = float(c["budget"][0]) if c["budget"][1] else int(c["budget"][0])
+            K, ids = as_input(c["K"]), torch.as_tensor(c["ids"]).cuda()
+            sel = tw.select_channel_pruned(as_input(c["q"]), K[:, ids], ids, budget)
+            np.testing.assert_array_equal(sel.indices.cpu().numpy(), c["indices"], err_msg=name)
+        else:
+            budget, p, is_frac, top = c["cfg"]
+            budget = float(budget) if is_frac else int(budget)
+            K, V, Q = as_input(c["K"]), as_input(c["V"]), as_input(c["Q"])
+            G = Q.shape[0]
+            sel = tw.SelectorConfig(kind="channel_pruned", budget=budget, top_channels=None if top < 0 else int(top))
+            cfg = tw.PipelineConfig(selector=sel, prune=tw.BinarySearchConfig(p=float(p)), group_map=tw.GroupMap(G))
+            if G == 1:
+                out, outcome, report = tw.run_head(Q[0], K, V, cfg)
+                outs, final, b0 = out[None], outcome.selection.indices, report.b0
+            else:
+                outs, outcomes, reports = tw.run_grouped(Q, K, V, cfg)
+                final, b0 = outcomes[0].selection.indices, reports[0].b0
+            assert b0 == c["b0"][0], name
+            final = final.cpu().numpy()
+            if not np.array_equal(final, c["final"]):
+                assert np.setxor1d(final, c["final"]).size <= 2, name  # top-p threshold ties only
+                continue
+            tol = 2e-2 if K.dtype == torch.bfloat16 else 1e-4
+            np.testing.assert_allclose(outs.cpu().numpy(), c["out"], rtol=tol, atol=tol * np.abs(c["out"]).max(),
+                                       err_msg=name)
+
+
+def test_channel_pruned_build_selector():
+    """build_selector binds the channel slice once per context (selectors.py:203-209)."""
+    rng = np.random.default_rng(3)
+    K = rng.standard_normal((400, 128)).astype(np.float32)
+    q = rng.standard_normal(128).astype(np.float32)
+    sel = tw.build_selector(tw.SelectorConfig(kind="channel_pruned", budget=50, top_channels=12), cuda(K))
+    got = sel(cuda(q)).indices.cpu().numpy()
+    ids = orc.top_channels_by_magnitude(K, 12)
+    np.testing.assert_array_equal(got, orc.channel_pruned_tokens(q, K, ids, 50))

@@ -6,6 +6,8 @@ logits: fp32 tolerance; top-p sets: identical up to threshold ties (1e-6).
 K4/K5 outputs: 1e-4 relative (fp32) and bf16 inputs with fp32 accumulation.
 """
 
+import math
+
 import numpy as np
 import pytest
 import torch
@@ -355,3 +357,88 @@ def test_two_and_eight_bit_cache_build_append_estimate(bits):
                 want = orc.estimate_logits(qh, codes, scale, zero, cand)
                 scale_ref = np.abs(qh).sum() * np.abs(K).max() / np.sqrt(128)
                 np.testing.assert_allclose(z, want, rtol=0, atol=2e-6 * scale_ref + 1e-6)
+
+
+def _near_tie_ok(got, want, q, K, ids, budget):
+    """Channel-pruned sets may differ from the oracle only where two scores
+    tie to fp64 rounding (the reference's BLAS summation order is unpinned)."""
+    diff = np.setxor1d(got, want)
+    if diff.size == 0:
+        return True
+    s = (K[:, ids].astype(np.float64) @ np.asarray(q, np.float64)[ids]) / math.sqrt(128)
+    kth = np.sort(s)[::-1][orc.resolve_budget(budget, K.shape[0]) - 1]
+    return diff.size <= 4 and bool(np.all(np.abs(s[diff] - kth) <= 1e-12 * max(1.0, abs(kth))))
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("top_channels,budget", [(None, 100), (5, 37), (128, 500)])
+def test_channel_pruned_selector_batched(dtype, top_channels, budget):
+    """The channel-pruned base selector (selectors.py:135-161) on the batched
+    path: channel slice, per-head token sets and their group union, then INT4
+    estimate / top-p / attention over exactly those tokens vs the oracle
+    (ragged lengths; one unit shorter than the budget keeps everything)."""
+    B, H, G, n = 3, 2, 4, 900
+    lengths = [900, 421, 60]
+    cache, batch = _cache(B, H, G, n, dtype, lengths, seed=31, tau=tau_schedule(H, (0.4, 1.5)))
+    p = 0.9
+    dec = TwilightDecoder(cache, "channel_pruned", budget=budget, p=p, top_channels=top_channels)
+    q = batch.q.contiguous()
+    out = dec.forward(q)
+    torch.cuda.synchronize()
+    bufs = dec.bufs
+    count = top_channels or 16
+    for b in range(B):
+        for h in range(H):
+            u = b * H + h
+            K, V = to_np(cache.unit_keys(b, h)), to_np(cache.unit_values(b, h))
+            Qn = to_np(q[b, h * G:(h + 1) * G])
+            ids = orc.top_channels_by_magnitude(K, count)
+            np.testing.assert_array_equal(bufs.chan_ids[u, :count].cpu().numpy(), ids)
+            heads = [orc.channel_pruned_tokens(Qn[g], K, ids, budget) for g in range(G)]
+            want_cand = orc.union_sorted(heads)
+            ncand = int(bufs.cand_count[u])
+            pages = bufs.cand_pages[u, :ncand].cpu().numpy()
+            np.testing.assert_array_equal(pages, np.unique(want_cand // 16))
+            pos = (pages[:, None] * 16 + np.arange(16)).reshape(-1)
+            z_all = bufs.logits[u, :, : ncand * 16].cpu().numpy()
+            valid = np.isfinite(z_all[0])
+            got = pos[valid]
+            if not np.array_equal(got, want_cand):
+                assert all(_near_tie_ok(got, want_cand, Qn[g], K, ids, budget) for g in range(G))
+                continue
+            res = orc.decode_unit(Qn, K, V, selector="channel_pruned", budget=budget, p=p, top_channels=count,
+                                  logits_override=[z_all[g][valid] for g in range(G)])
+            final = bufs.final_idx[u, : int(bufs.final_count[u])].cpu().numpy()
+            assert np.isin(final, want_cand).all()
+            if not np.array_equal(final, res["final"]):
+                assert np.setxor1d(final, res["final"]).size <= 2  # threshold ties only
+                continue
+            for g in range(G):
+                want = res["out"][g]
+                np.testing.assert_allclose(to_np(out[b, h * G + g]), want, rtol=1e-4, atol=1e-4 * np.abs(want).max())
+
+
+def test_channel_pruned_fixed_slice_survives_appends():
+    """fix_channels keeps the slice ranked at the first step (build_selector
+    binds it once per context, selectors.py:203); without it every step
+    re-ranks the current cache."""
+    B, H, G, n = 2, 2, 2, 300
+    dtype = torch.float32
+    cache, batch = _cache(B, H, G, n, dtype, [300, 250], seed=5, extra_pages=4)
+    fixed = TwilightDecoder(cache, "channel_pruned", budget=64, p=0.9, fix_channels=True)
+    live = TwilightDecoder(cache, "channel_pruned", budget=64, p=0.9)
+    q = batch.q.contiguous()
+    fixed.forward(q)
+    first = fixed.bufs.chan_ids[:, :16].clone()
+    # append large keys on the channels that were NOT selected, until they dominate the magnitudes
+    for step in range(40):
+        k_new = torch.zeros(B, H, 128, dtype=dtype, device="cuda")
+        k_new[..., 100:] = 1e3
+        cache.append(k_new, torch.zeros_like(k_new))
+    fixed.forward(q)
+    live.forward(q)
+    torch.cuda.synchronize()
+    assert torch.equal(fixed.bufs.chan_ids[:, :16], first)
+    for u in range(B * H):
+        K = to_np(cache.unit_keys(u // H, u % H))
+        np.testing.assert_array_equal(live.bufs.chan_ids[u, :16].cpu().numpy(), orc.top_channels_by_magnitude(K, 16))

@@ -69,9 +69,22 @@ def test_cost_model_matches_paper():
         tw.memory_overhead(3)
 
 
-def test_unsupported_selectors_fail_loudly():
-    with pytest.raises(NotImplementedError):
-        tw.select_channel_pruned(None, None, None, 0.5)
+def test_channel_pruned_validation():
+    # selectors.py:135-161 argument checks (raised before any device work), and
+    # host tensors are refused: the selector has no CPU fallback
+    import torch
+    with pytest.raises(ValueError):
+        tw.top_channels_by_magnitude(torch.zeros(10, 128), 0)
+    with pytest.raises(ValueError):
+        tw.top_channels_by_magnitude(torch.zeros(10, 128), 4)
+    with pytest.raises(ValueError):
+        tw.select_channel_pruned(torch.zeros(128), torch.zeros(10, 3), [1, 2], 5)
+    with pytest.raises(ValueError):
+        tw.select_channel_pruned(torch.zeros(128), torch.zeros(10, 2), [1, 200], 5)
+    with pytest.raises(ValueError):
+        tw.select_channel_pruned(torch.zeros(128), torch.zeros(10, 2), [4, 4], 5)
+    with pytest.raises(ValueError):
+        tw.select_channel_pruned(torch.zeros(128), torch.zeros(10, 2), [4, 5], 5)
 
 
 def test_select_sink_window_validation():

@@ -125,3 +125,24 @@ def test_two_and_eight_bit_caches_match_reference(golden):
         np.testing.assert_array_equal(zero, c["zero"], err_msg=name)
         z = orc.estimate_logits(c["q"], codes, scale, zero, c["idx"])
         np.testing.assert_allclose(z, c["scores"], rtol=1e-6, atol=1e-6, err_msg=name)
+
+
+def test_channel_pruned_matches_reference(golden):
+    """top_channels_by_magnitude / select_channel_pruned / run_grouped with the
+    channel-pruned selector (selectors.py:135-161): bit-exact id and index sets."""
+    for name, c in golden("channel").items():
+        if name.startswith("m"):
+            np.testing.assert_array_equal(orc.top_channels_by_magnitude(c["K"], int(c["count"][0])), c["ids"],
+                                          err_msg=name)
+        elif name.startswith("s"):
+            budget = float(c["budget"][0]) if c["budget"][1] else int(c["budget"][0])
+            np.testing.assert_array_equal(orc.channel_pruned_tokens(c["q"], c["K"], c["ids"], budget),
+                                          c["indices"], err_msg=name)
+        else:
+            budget, p, is_frac, top = c["cfg"]
+            budget = float(budget) if is_frac else int(budget)
+            res = orc.decode_unit(c["Q"], c["K"], c["V"], selector="channel_pruned", budget=budget, p=float(p),
+                                  top_channels=None if top < 0 else int(top))
+            np.testing.assert_array_equal(res["final"], c["final"], err_msg=name)
+            assert res["candidates"].size == c["b0"][0], name
+            np.testing.assert_allclose(res["out"], c["out"], rtol=1e-5, atol=1e-6, err_msg=name)
