@@ -26,7 +26,13 @@
 
 namespace tw {
 
-constexpr int kEstPagesPerCta = 32;  // candidate pages per work item (one per lane)
+#ifndef TW_EST_ITEM
+#define TW_EST_ITEM 32
+#endif
+#ifndef TW_EST_STAGES
+#define TW_EST_STAGES 4
+#endif
+constexpr int kEstPagesPerCta = TW_EST_ITEM;  // candidate pages per work item (<= 32: one per lane)
 constexpr int kEstWarps = 4;
 
 __device__ __forceinline__ void mma_u8s8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -38,7 +44,7 @@ __device__ __forceinline__ void mma_u8s8(int (&c)[4], const uint32_t (&a)[4], ui
 }
 
 constexpr int kDigits = 3;         // q as 3 signed base-256 digits of a 22-bit fixed-point value
-constexpr int kEstStages = 4;      // pages in flight per warp (cp.async ring)
+constexpr int kEstStages = TW_EST_STAGES;  // pages in flight per warp (cp.async ring)
 
 // vector loads of 4 / 32 consecutive q elements as float
 __device__ __forceinline__ void load4(const __nv_bfloat16* p, float& a, float& b, float& c, float& d) {
@@ -192,11 +198,13 @@ template <typename T, int G, int BITS>
 __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv, const T* __restrict__ q,
                                                                   tw_decode_buffers buf, int max_chunks,
                                                                   int sw_sink, int sw_window,
-                                                                  const uint32_t* __restrict__ tok_mask) {
+                                                                  const uint32_t* __restrict__ tok_mask,
+                                                                  int item) {
   pdl_wait();
   pdl_trigger();
+  constexpr int kSt = BITS == 8 && kEstStages > 4 ? 4 : kEstStages;  // 8-bit blocks: static smem cap
   constexpr int kBlock = qblock_bytes_for(BITS), kCodes = code_bytes_for(BITS), kRowBytes = kHeadDim * BITS / 8;
-  __shared__ __align__(128) uint8_t ring[kEstWarps][kEstStages][kBlock];
+  __shared__ __align__(128) uint8_t ring[kEstWarps][kSt][kBlock];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane & 3, r = lane >> 2;
   const int units = kv.num_seqs * kv.num_kv_heads;
@@ -217,8 +225,7 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
       if (r == 0 && t < G && mx > -INFINITY) atomicMax(buf.head_max + (size_t)u * G + t, f2key(mx));
       run_max[0] = -INFINITY;
-      return;
-    }
+    } else {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       float mx = run_max[e];
@@ -229,15 +236,16 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       if (r == 0 && g < G && mx > -INFINITY) atomicMax(buf.head_max + (size_t)u * G + g, f2key(mx));
       run_max[e] = -INFINITY;
     }
+    }
   };
   for (int it = warp_fetch(buf.counters + 3); it < units * max_chunks; it = warp_fetch(buf.counters + 3)) {
     const int unit = it % units;  // chunk-major: non-empty items come first, spread over all warps
-    const int c0 = (it / units) * kEstPagesPerCta;
+    const int c0 = (it / units) * item;
     const int ncand = buf.cand_count[unit];
     if (c0 >= ncand) continue;
     const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
     const int n = kv.seq_lens[b];
-    const int np = min(kEstPagesPerCta, ncand - c0);
+    const int np = min(item, ncand - c0);
     // candidate page -> physical block, one page per lane
     int lp_l = 0;
     const uint8_t* src_l = kv.kq;
@@ -247,12 +255,12 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
     }
     auto issue = [&](int i) {
       const uint8_t* src = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, (unsigned long long)src_l, i));
-      uint8_t* dst = R[i % kEstStages];
+      uint8_t* dst = R[i % kSt];
 #pragma unroll
       for (int c = lane; c < kBlock / 16; c += 32) cp_async16(dst + 16 * c, src + 16 * c);
     };
 #pragma unroll
-    for (int i = 0; i < kEstStages - 1; ++i) {
+    for (int i = 0; i < kSt - 1; ++i) {
       if (i < np) issue(i);
       cp_commit();
     }
@@ -263,11 +271,11 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       cur_unit = unit;
     }
     for (int i = 0; i < np; ++i) {
-      if (i + kEstStages - 1 < np) issue(i + kEstStages - 1);
+      if (i + kSt - 1 < np) issue(i + kSt - 1);
       cp_commit();
-      cp_wait<kEstStages - 1>();
+      cp_wait<kSt - 1>();
       __syncwarp();
-      const uint8_t* pg = R[i % kEstStages];
+      const uint8_t* pg = R[i % kSt];
       // the lane's code bytes of rows r and r+8: channels 32t .. 32t+31
       uint32_t wl[BITS], wh[BITS];
       if (BITS == 8) {
@@ -422,16 +430,21 @@ using namespace tw;
 template <typename T, int G, int BITS>
 static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, int sw_sink,
                               int sw_window, const uint32_t* tok_mask, cudaStream_t stream) {
-  const int max_chunks = (kv->max_pages + kEstPagesPerCta - 1) / kEstPagesPerCta;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, estimate_kernel<T, G, BITS>, kEstWarps * 32, 0);
-  const int items = kv->num_seqs * kv->num_kv_heads * max_chunks;
   int grid = sms * persist_cap(per_sm);
+  // item size: 32 pages (amortises the per-item index lookups and ring fill) unless
+  // that leaves warps idle -- small batches split into 16- or 8-page items
+  const int units = kv->num_seqs * kv->num_kv_heads;
+  int item = kEstPagesPerCta;
+  while (item > 8 && (long long)units * ((kv->max_pages + item - 1) / item) < (long long)grid * kEstWarps) item /= 2;
+  const int max_chunks = (kv->max_pages + item - 1) / item;
+  const int items = units * max_chunks;
   if (grid * kEstWarps > items) grid = (items + kEstWarps - 1) / kEstWarps;
   launch_pdl(estimate_kernel<T, G, BITS>, dim3(grid), dim3(kEstWarps * 32), 0, stream, *kv, q, *buf, max_chunks, sw_sink,
-             sw_window, tok_mask);
+             sw_window, tok_mask, item);
 }
 
 template <typename T>
