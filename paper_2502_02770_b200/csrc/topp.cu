@@ -298,9 +298,13 @@ struct UnitCfg {
   static constexpr size_t kHistBytes = (size_t)GB * kBins * 8;
   static constexpr size_t kResBytes = (size_t)GB * sizeof(ResGroupSmem);
   static constexpr size_t kSmem = (kHistBytes > kResBytes ? kHistBytes : kResBytes) + (size_t)MC * 8;
+  // the union bitmap lives in the histogram region (dead after the crossing
+  // scan) behind the resolve scratch, when the context fits
+  static constexpr size_t kBitsOff = (kResBytes + 15) & ~size_t(15);
+  static constexpr size_t kBitsCap = kHistBytes > kBitsOff ? (kHistBytes - kBitsOff) / 4 : 0;  // words
 };
 
-template <int G, int HB>
+template <int G, int HB, bool SB>
 __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_kv kv, tw_decode_params prm,
                                                                       tw_decode_buffers buf) {
   pdl_wait();
@@ -325,7 +329,13 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
   const int npos = buf.cand_count[unit] * kPage;
   const int n4 = npos >> 2;
   const float* zu = buf.logits + (size_t)unit * G * T;
-  uint32_t* ubits = buf.sel_bits + (size_t)unit * ((T + 31) / 32);
+  // SB: the bitmap in shared memory (pass 2 writes every word it covers, so no zeroing)
+  uint32_t* ubits = SB ? reinterpret_cast<uint32_t*>(sm + Cfg::kBitsOff)
+                       : buf.sel_bits + (size_t)unit * ((T + 31) / 32);
+  auto ld_bits = [&](int w) -> uint32_t {
+    if constexpr (SB) return ubits[w];
+    else return __ldcg(ubits + w);
+  };
   const double p_eff = fmin(prm.p, 1.0) - 1e-9;
   if (tid < G) {
     const float M = key2f(buf.head_max[(size_t)unit * G + tid]);  // NaN when the head has no valid logit
@@ -578,7 +588,7 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
     }
     grp.sync();
   }
-  __syncthreads();  // member bits (global atomics of this CTA) are visible to its ld.cg below
+  __syncthreads();  // member bits (atomics of this CTA) are visible to the loads below
   TT(4);
 
   // ---- K3c: compact the union bitmap -> ascending token ids + attention work items.
@@ -593,7 +603,7 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
   const int per_w = (words + NW - 1) / NW;
   const int wlo = min(words, warp * per_w), whi = min(words, wlo + per_w);
   uint32_t cnt = 0;
-  for (int w = wlo + lane; w < whi; w += 32) cnt += __popc(__ldcg(ubits + w));
+  for (int w = wlo + lane; w < whi; w += 32) cnt += __popc(ld_bits(w));
   cnt = warp_sum(cnt);
   if (lane == 0) s_wtot[warp] = cnt;
   __syncthreads();
@@ -603,9 +613,16 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
     run += i < warp ? s_wtot[i] : 0u;
     basei += s_wtot[i];
   }
+  // claim the unit's attention work items now: the atomic's latency overlaps the emission
+  const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : TW_DEFAULT_CHUNK;
+  const int nitems = ((int)basei + chunk - 1) / chunk;
+  if (tid == 0) {
+    buf.final_count[unit] = (int)basei;
+    s_first = nitems ? (int)atomicAdd(&buf.counters[0], (uint32_t)nitems) : 0;
+  }
   for (int w0 = wlo; w0 < whi; w0 += 32) {
     const int w = w0 + lane;
-    const uint32_t x = w < whi ? __ldcg(ubits + w) : 0u;
+    const uint32_t x = w < whi ? ld_bits(w) : 0u;
     const int pa = 2 * w0 + lane < kv.max_pages ? cand[2 * w0 + lane] : 0;
     const int pb = 2 * w0 + 32 + lane < kv.max_pages ? cand[2 * w0 + 32 + lane] : 0;
     uint32_t incl = __popc(x);
@@ -627,15 +644,11 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
     run += __shfl_sync(0xffffffffu, incl, 31);
   }
   TT(5);
-  const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : TW_DEFAULT_CHUNK;
-  const int nitems = ((int)basei + chunk - 1) / chunk;
+  __syncthreads();
   if (tid == 0) {
-    buf.final_count[unit] = (int)basei;
-    s_first = nitems ? (int)atomicAdd(&buf.counters[0], (uint32_t)nitems) : 0;
     buf.unit_items[2 * unit] = s_first;
     buf.unit_items[2 * unit + 1] = nitems;
   }
-  __syncthreads();
   for (int i = tid; i < nitems; i += NT) {
     if (s_first + i < buf.max_items) {
       buf.work_items[2 * (s_first + i)] = unit;
@@ -999,16 +1012,24 @@ extern "C" int tw_debug_ttrace(unsigned long long* host_out) {
 }
 #endif
 
+template <int G, int HB, bool SB>
+static int launch_unit_sb(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,
+                          cudaStream_t stream) {
+  const size_t smem = UnitCfg<G, HB>::kSmem;
+  if (cudaFuncSetAttribute(topp_unit_kernel<G, HB, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return TW_ERR_CUDA;
+  launch_pdl(topp_unit_kernel<G, HB, SB>, dim3(kv->num_seqs * kv->num_kv_heads), dim3(UnitCfg<G, HB>::NT), smem,
+             stream, *kv, *prm, *buf);
+  return launch_status();
+}
+
 template <int G, int HB>
 static int launch_unit_hb(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,
                           cudaStream_t stream) {
-  const size_t smem = UnitCfg<G, HB>::kSmem;
-  if (cudaFuncSetAttribute(topp_unit_kernel<G, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return TW_ERR_CUDA;
-  launch_pdl(topp_unit_kernel<G, HB>, dim3(kv->num_seqs * kv->num_kv_heads), dim3(UnitCfg<G, HB>::NT), smem, stream,
-             *kv, *prm, *buf);
-  return launch_status();
+  const size_t words = ((size_t)kv->max_pages * kPage + 31) / 32;
+  if (words <= UnitCfg<G, HB>::kBitsCap) return launch_unit_sb<G, HB, true>(kv, prm, buf, stream);
+  return launch_unit_sb<G, HB, false>(kv, prm, buf, stream);
 }
 
 template <int G>

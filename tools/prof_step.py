@@ -31,6 +31,7 @@ dec = TwilightDecoder(cache, cfg["selector"], budget=cfg["budget"], p=cfg["p"])
 q = batch.q.contiguous()
 pos = torch.full((B,), n - 1, dtype=torch.int32, device="cuda")
 out = torch.empty(B, H * G, 128, device="cuda")
+from paper_2502_02770_b200 import _lib as _lib0  # noqa: E402
 for _ in range(args.reps):
     cache.append(batch.k_new, batch.v_new, pos)
     dec.select(q)
@@ -39,18 +40,14 @@ for _ in range(args.reps):
     dec.attend(q, out)
     if args.dense:
         dec.dense(q, out)
+    if _ < args.reps - 1 and hasattr(_lib0.lib(), "tw_debug_strace"):  # keep the last (warm) step's trace
+        import ctypes
+        _lib0.lib().tw_debug_strace((ctypes.c_ulonglong * (512 * 16))())
 torch.cuda.synchronize()
-if os.environ.get("TW_LIB_PATH") and hasattr(__import__("paper_2502_02770_b200._lib", fromlist=["lib"]).lib(), "tw_debug_trace"):
+if os.environ.get("TW_LIB_PATH") and hasattr(__import__("paper_2502_02770_b200._lib", fromlist=["lib"]).lib(), "tw_debug_strace"):
     import ctypes
     import numpy as np
     from paper_2502_02770_b200 import _lib
-    buf = (ctypes.c_ulonglong * (512 * 8))()
-    _lib.lib().tw_debug_trace(buf)
-    a = np.frombuffer(buf, dtype=np.uint64).reshape(512, 8).astype(np.int64)
-    d = np.diff(a, axis=1)
-    print("phase durations us (mean over heads):", (d.mean(axis=0) / 1000).round(2).tolist())
-    print("phase durations us (max):", (d.max(axis=0) / 1000).round(2).tolist())
-    print("kernel span us:", (a[:, 6].max() - a[:, 0].min()) / 1000)
     buf2 = (ctypes.c_ulonglong * (512 * 16))()
     _lib.lib().tw_debug_strace(buf2)
     s = np.frombuffer(buf2, dtype=np.uint64).reshape(512, 16).astype(np.int64)
@@ -60,6 +57,7 @@ if os.environ.get("TW_LIB_PATH") and hasattr(__import__("paper_2502_02770_b200._
     d = np.diff(s[:, :nph], axis=1)
     print("select phases us (mean):", (d.mean(axis=0) / 1000).round(2).tolist())
     print("select phases us (max):", (d.max(axis=0) / 1000).round(2).tolist())
+    print("select span us:", (s[:, nph - 1].max() - s[:, 0].min()) / 1000)
 st = dec.stats()
 print("cand tokens/unit", float(st.cand_pages.float().mean()) * 16, "final/unit", float(st.group_b1.float().mean()),
       "rescored pages", int(dec.bufs.counters[1]))
