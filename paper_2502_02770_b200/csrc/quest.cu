@@ -46,7 +46,7 @@ constexpr int kSelThreads = 512;
 #ifndef TW_QF_ITEM
 #define TW_QF_ITEM 64
 #endif
-constexpr int kFilterPagesPerCta = TW_QF_ITEM;
+constexpr int kFilterPagesPerCta = TW_QF_ITEM;  // largest filter item (<= 64: two pages per lane)
 
 // ---------------------------------------------------------------- filter pass
 
@@ -60,7 +60,7 @@ constexpr int kQfStages = 4;
 template <typename T, int G>
 __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_kernel(tw_paged_kv kv, const T* __restrict__ q,
                                                                      float* __restrict__ scores, int max_chunks,
-                                                                     uint32_t* __restrict__ ctr) {
+                                                                     uint32_t* __restrict__ ctr, int item) {
   __shared__ __align__(128) T ring[kQfWarps][kQfStages][2][2 * kHeadDim];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane & 15, half = lane >> 4;
@@ -72,11 +72,11 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_kernel(tw_paged_kv
   int cur_unit = -1;
   for (int it = warp_fetch(ctr); it < units * max_chunks; it = warp_fetch(ctr)) {
     const int unit = it % units;
-    const int p0 = (it / units) * kFilterPagesPerCta;
+    const int p0 = (it / units) * item;
     const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
     const int npages = (kv.seq_lens[b] + kPage - 1) / kPage;
     if (p0 >= npages) continue;
-    const int np = min(kFilterPagesPerCta, npages - p0);
+    const int np = min(item, npages - p0);
     const int* pt = kv.page_table + (size_t)b * kv.max_pages;
     // physical metadata blocks of pages p0 + lane and p0 + 32 + lane
     const T* src0 = reinterpret_cast<const T*>(kv.kmeta);
@@ -169,7 +169,7 @@ template <int G>
 __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_paged_kv kv,
                                                                          const __nv_bfloat16* __restrict__ q,
                                                                          float* __restrict__ scores, int max_chunks,
-                                                                         uint32_t* __restrict__ ctr) {
+                                                                         uint32_t* __restrict__ ctr, int item) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(128) uint8_t qm_ring[];
@@ -181,11 +181,11 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
   int cur_unit = -1;
   for (int it = warp_fetch(ctr); it < units * max_chunks; it = warp_fetch(ctr)) {
     const int unit = it % units;
-    const int p0 = (it / units) * kFilterPagesPerCta;
+    const int p0 = (it / units) * item;
     const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
     const int npages = (kv.seq_lens[b] + kPage - 1) / kPage;
     if (p0 >= npages) continue;
-    const int np = min(kFilterPagesPerCta, npages - p0);
+    const int np = min(item, npages - p0);
     const int* pt = kv.page_table + (size_t)b * kv.max_pages;
     const uint8_t* base = reinterpret_cast<const uint8_t*>(kv.kmeta);
     const uint8_t* src0 = base;
@@ -509,10 +509,14 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
   const int units = kv->num_seqs * kv->num_kv_heads;
   cudaMemsetAsync(buf->counters, 0, 8 * sizeof(uint32_t), stream);
   if (prm->selector == TW_SELECT_QUEST) {
-    const int max_chunks = (kv->max_pages + kFilterPagesPerCta - 1) / kFilterPagesPerCta;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // item size: 64 pages, halved (to 16 at least) while units x chunks would leave warps idle
+    int item = kFilterPagesPerCta;
+    while (item > 16 && (long long)units * ((kv->max_pages + item - 1) / item) < (long long)sms * 3 * kQfWarps)
+      item /= 2;
+    const int max_chunks = (kv->max_pages + item - 1) / item;
     const int items = units * max_chunks;
     const T* qq = (const T*)q;
     auto go = [&](auto kern) {
@@ -520,7 +524,7 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQfWarps * 32, 0);
       int grid = sms * persist_cap(per_sm);
       if (grid * kQfWarps > items) grid = (items + kQfWarps - 1) / kQfWarps;
-      kern<<<grid, kQfWarps * 32, 0, stream>>>(*kv, qq, buf->page_scores, max_chunks, buf->counters + 2);
+      kern<<<grid, kQfWarps * 32, 0, stream>>>(*kv, qq, buf->page_scores, max_chunks, buf->counters + 2, item);
     };
     if constexpr (sizeof(T) == 2) {
       auto gom = [&](auto kern) {
@@ -531,7 +535,7 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
         int grid = sms * persist_cap(per_sm);
         if (grid * kQfWarps > items) grid = (items + kQfWarps - 1) / kQfWarps;
         launch_pdl(kern, dim3(grid), dim3(kQfWarps * 32), smem, stream, *kv, (const __nv_bfloat16*)q,
-                   buf->page_scores, max_chunks, buf->counters + 2);
+                   buf->page_scores, max_chunks, buf->counters + 2, item);
       };
       switch (kv->group_size) {
         case 1: gom(quest_filter_mma_kernel<1>); break;
