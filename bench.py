@@ -418,7 +418,9 @@ def run_ours(args, cfg):
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us/layer", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "path": "tw_decode_step C-ABI call (captured), q/k_new/v_new from pinned host, out to pinned host"},
-        "gpu_launches": (7 if cfg["selector"] == "quest" else 6) * args.steps,  # append, [filter], select, estimate, top-p, attention, merge
+        # quest: filter (+ fused K1 append), select, estimate, top-p, attention, merge;
+        # other selectors: append, select, estimate, top-p, attention, merge
+        "gpu_launches": 6 * args.steps,
         "roofline": {"bound": "hbm", "kernel": dominant,
                      "achieved": round(kernel_gbs[dominant], 1) if kernel_gbs[dominant] else None,
                      "peak": peak, "unit": "GB/s",
@@ -588,7 +590,7 @@ def run_model(args, cfg):
         "e2e": {"value": round(e2e_ms * 1e3 / L, 2), "unit": "us/layer", "h2d_bytes_per_step": B * 8,
                 "d2h_bytes_per_step": B * 8,
                 "path": "LlamaTwilightDecoder.step (captured) with token ids from pinned host, argmax ids to host"},
-        "gpu_launches": (8 * n_tw + 3 * n_dense) * args.steps,
+        "gpu_launches": ((7 if cfg["selector"] == "quest" else 8) * n_tw + 3 * n_dense) * args.steps,
         "roofline": {"bound": "hbm", "kernel": dominant,
                      "achieved": round(kernel_gbs[dominant], 1) if kernel_gbs[dominant] else None,
                      "peak": peak, "unit": "GB/s",

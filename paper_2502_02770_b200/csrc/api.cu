@@ -3,12 +3,19 @@
 
 extern "C" int32_t tw_version(void) { return 100; }  // 0.1.0
 
+int tw_select_append(const tw_paged_kv* kv, const void* q, const void* k_new, const void* v_new,
+                     const int32_t* positions, const tw_decode_params* prm, const tw_decode_buffers* buf,
+                     cudaStream_t stream);  // quest.cu
+
 extern "C" int tw_decode_step(const tw_paged_kv* kv, const void* q, const void* k_new, const void* v_new,
                               const int32_t* positions, const tw_decode_params* prm,
                               const tw_decode_buffers* buf, float* out, cudaStream_t stream) {
-  int s;
-  if ((s = tw_quant_append(kv, k_new, v_new, positions, stream))) return s;
-  if ((s = tw_select(kv, q, prm, buf, stream))) return s;
+  int s = tw_select_append(kv, q, k_new, v_new, positions, prm, buf, stream);  // K1 fused into the Quest filter
+  if (s == 1) {
+    if ((s = tw_quant_append(kv, k_new, v_new, positions, stream))) return s;
+    s = tw_select(kv, q, prm, buf, stream);
+  }
+  if (s) return s;
   if ((s = tw_estimate(kv, q, prm, buf, stream))) return s;
   if ((s = tw_topp(kv, prm, buf, stream))) return s;
   return tw_sparse_attention(kv, q, prm, buf, out, stream);

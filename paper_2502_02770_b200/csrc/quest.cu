@@ -16,6 +16,7 @@
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), see oracle.numpy_rowsum_order) and
 // ranked by (score desc, page asc).  The result is the reference's page set.
 #include "block_scan.cuh"
+#include "quant_row.cuh"
 
 #ifdef TW_TOPP_TRACE
 __device__ unsigned long long g_strace[512 * 16];
@@ -165,11 +166,17 @@ __device__ __forceinline__ void mma_bf16_q(float (&c)[4], const uint32_t (&a)[4]
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// With `positions` (the fused decode step) the warp whose item holds a unit's
+// open page first appends that unit's new row (K1, append_row_warp) and then
+// streams the page's updated metadata; page counts come from positions + 1.
 template <int G>
 __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_paged_kv kv,
                                                                          const __nv_bfloat16* __restrict__ q,
                                                                          float* __restrict__ scores, int max_chunks,
-                                                                         uint32_t* __restrict__ ctr, int item) {
+                                                                         uint32_t* __restrict__ ctr, int item,
+                                                                         const __nv_bfloat16* __restrict__ k_new,
+                                                                         const __nv_bfloat16* __restrict__ v_new,
+                                                                         const int32_t* __restrict__ positions) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(128) uint8_t qm_ring[];
@@ -183,9 +190,20 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
     const int unit = it % units;
     const int p0 = (it / units) * item;
     const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
-    const int npages = (kv.seq_lens[b] + kPage - 1) / kPage;
+    const int n = positions ? __ldg(positions + b) + 1 : kv.seq_lens[b];
+    const int npages = (n + kPage - 1) / kPage;
     if (p0 >= npages) continue;
     const int np = min(item, npages - p0);
+    if (positions && npages - 1 < p0 + np) {  // this item holds the open page: append first
+      switch (kv.bits) {
+        case 2: append_row_warp<__nv_bfloat16, 2>(kv, b, h, lane, k_new, v_new, n - 1); break;
+        case 8: append_row_warp<__nv_bfloat16, 8>(kv, b, h, lane, k_new, v_new, n - 1); break;
+        default: append_row_warp<__nv_bfloat16, 4>(kv, b, h, lane, k_new, v_new, n - 1); break;
+      }
+      if (h == 0 && lane == 0) kv.seq_lens[b] = n;  // every reader in this kernel uses positions
+      __threadfence();  // the metadata stores precede this warp's cp.async reads of the page
+      __syncwarp();
+    }
     const int* pt = kv.page_table + (size_t)b * kv.max_pages;
     const uint8_t* base = reinterpret_cast<const uint8_t*>(kv.kmeta);
     const uint8_t* src0 = base;
@@ -505,7 +523,8 @@ using namespace tw;
 
 template <typename T>
 static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
-                         const tw_decode_buffers* buf, cudaStream_t stream) {
+                         const tw_decode_buffers* buf, cudaStream_t stream, const void* k_new = nullptr,
+                         const void* v_new = nullptr, const int32_t* positions = nullptr) {
   const int units = kv->num_seqs * kv->num_kv_heads;
   cudaMemsetAsync(buf->counters, 0, 8 * sizeof(uint32_t), stream);
   if (prm->selector == TW_SELECT_QUEST) {
@@ -535,7 +554,8 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
         int grid = sms * persist_cap(per_sm);
         if (grid * kQfWarps > items) grid = (items + kQfWarps - 1) / kQfWarps;
         launch_pdl(kern, dim3(grid), dim3(kQfWarps * 32), smem, stream, *kv, (const __nv_bfloat16*)q,
-                   buf->page_scores, max_chunks, buf->counters + 2, item);
+                   buf->page_scores, max_chunks, buf->counters + 2, item, (const __nv_bfloat16*)k_new,
+                   (const __nv_bfloat16*)v_new, positions);
       };
       switch (kv->group_size) {
         case 1: gom(quest_filter_mma_kernel<1>); break;
@@ -563,6 +583,23 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
 
 int tw_select_channel_pruned(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
                              const tw_decode_buffers* buf, cudaStream_t stream);  // channel.cu
+
+// The decode step's K1 + K2 in one pass when the Quest filter runs on the bf16
+// tensor-core kernel: returns 1 (nothing launched) when the step must append
+// separately (fp32 cache, other selectors, all-pages budget).
+int tw_select_append(const tw_paged_kv* kv, const void* q, const void* k_new, const void* v_new,
+                     const int32_t* positions, const tw_decode_params* prm, const tw_decode_buffers* buf,
+                     cudaStream_t stream) {
+  if (!kv || !prm || !buf || !k_new || !v_new || !positions || kv->dtype != TW_BF16 ||
+      prm->selector != TW_SELECT_QUEST || kv->head_dim != kHeadDim || kv->num_kv_heads < 1 ||
+      kv->num_kv_heads > 32 || kv->num_seqs < 1 || kv->max_pages < 1 ||
+      (kv->group_size != 1 && kv->group_size != 2 && kv->group_size != 4 && kv->group_size != 8) ||
+      (kv->bits != 0 && kv->bits != 2 && kv->bits != 4 && kv->bits != 8) || prm->budget_pages < 1 ||
+      !buf->page_scores || !buf->band_idx || !buf->band_scores || !q || !buf->cand_pages || !buf->cand_count ||
+      !buf->counters || !buf->head_max)
+    return 1;
+  return launch_select<__nv_bfloat16>(kv, q, prm, buf, stream, k_new, v_new, positions);
+}
 
 extern "C" int tw_select(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
                          const tw_decode_buffers* buf, cudaStream_t stream) {

@@ -442,3 +442,36 @@ def test_channel_pruned_fixed_slice_survives_appends():
     for u in range(B * H):
         K = to_np(cache.unit_keys(u // H, u % H))
         np.testing.assert_array_equal(live.bufs.chan_ids[u, :16].cpu().numpy(), orc.top_channels_by_magnitude(K, 16))
+
+
+@pytest.mark.parametrize("bits", [4, 2, 8])
+def test_fused_step_append_matches_separate_append(bits):
+    """tw_decode_step fuses K1 into the Quest filter (the warp holding a unit's
+    open page appends first): over several steps -- opening new pages -- the
+    cache (rows, codes, params, page metadata, |k| bound, lengths) and the
+    outputs equal the separate append kernel followed by the staged path."""
+    B, H, G, n = 2, 2, 4, 700
+    dtype = torch.bfloat16
+    lengths = [638, 511]
+    batch = make_batch(B, H, G, n, dtype, tau=0.7, seed=77)
+    caches = []
+    for _ in range(2):
+        c = PagedKVCache(B, H, G, max_pages=pages_for(n) + 2, dtype=dtype, bits=bits)
+        c.prefill(batch.K, batch.V, lengths)
+        caches.append(c)
+    fused = TwilightDecoder(caches[0], "quest", budget=160, p=0.9)
+    staged = TwilightDecoder(caches[1], "quest", budget=160, p=0.9)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    for step in range(20):
+        k_new = torch.randn(B, H, 128, device="cuda", generator=gen).to(dtype)
+        v_new = torch.randn(B, H, 128, device="cuda", generator=gen).to(dtype)
+        q = (torch.randn(B, H * G, 128, device="cuda", generator=gen) * 0.5).to(dtype)
+        out_f = fused.step(q, k_new, v_new)
+        caches[1].append(k_new, v_new)
+        out_s = staged.forward(q)
+        torch.cuda.synchronize()
+        assert torch.equal(out_f, out_s), step
+    a, c = caches
+    assert a.seq_lens.tolist() == c.seq_lens.tolist() == [658, 531]
+    for name in ("k_cache", "v_cache", "kq", "kmeta", "kabsmax"):
+        assert torch.equal(getattr(a, name), getattr(c, name)), name
