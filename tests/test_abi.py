@@ -65,6 +65,19 @@ def test_invalid_arguments_are_rejected_without_a_gpu():
     buf = _lib.TwDecodeBuffers()
     assert lib.tw_topp(ctypes.byref(kv), ctypes.byref(prm), ctypes.byref(buf), None) == _lib.TW_ERR_INVALID
     assert lib.tw_max_work_items(ctypes.byref(kv), 512) == 1
+    # channel-pruned selector (csrc/channel.cu): argument checks precede any launch
+    kv.group_size, kv.dtype = 4, _lib.TW_BF16
+    prm.selector, prm.budget_tokens = _lib.TW_SELECT_CHANNEL_PRUNED, 64
+    assert lib.tw_select(ctypes.byref(kv), None, ctypes.byref(prm), ctypes.byref(buf), None) == _lib.TW_ERR_INVALID
+    fake = ctypes.c_void_p(256)
+    for name in ("cand_pages", "cand_count", "logits", "tok_mask", "chan_ids", "head_max", "counters"):
+        setattr(buf, name, fake)
+    kv.max_pages = 4096  # 65536 tokens: beyond the selector's 32768-token shared-memory key array
+    assert lib.tw_select(ctypes.byref(kv), fake, ctypes.byref(prm), ctypes.byref(buf), None) == _lib.TW_ERR_INVALID
+    kv.max_pages, prm.top_channels = 4, 129
+    assert lib.tw_select(ctypes.byref(kv), fake, ctypes.byref(prm), ctypes.byref(buf), None) == _lib.TW_ERR_INVALID
+    prm.top_channels, prm.budget_tokens = 16, 0
+    assert lib.tw_select(ctypes.byref(kv), fake, ctypes.byref(prm), ctypes.byref(buf), None) == _lib.TW_ERR_INVALID
 
 
 def test_status_codes_map_to_reference_exceptions():
