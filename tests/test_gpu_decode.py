@@ -82,14 +82,18 @@ def test_k1_append_equals_bulk(dtype):
 
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("page_local", [False, True])
-def test_k2_quest_pages_bit_exact(dtype, page_local):
-    B, H, G, n = 2, 2, 4, 1000
-    lengths = [1000, 777]
+@pytest.mark.parametrize("B", [2, 20])
+def test_k2_quest_pages_bit_exact(dtype, page_local, B):
+    """Page sets per head and their union, bit-exact vs the oracle, for a
+    small batch and one with more (unit, head) pairs than SMs."""
+    H, G, n = 2, 4, 1000
+    lengths = [1000, 777] * (B // 2)
     cache, batch = _cache(B, H, G, n, dtype, lengths, seed=3, tau=0.5, page_local=page_local)
     budget = 256
     dec = TwilightDecoder(cache, "quest", budget=budget, p=0.95, head_page_bits=True)
     q = batch.q.contiguous()
     dec.select(q)
+    dec.select(q)  # a second step over the same buffers
     # exact fp64 page bounds, bit-identical to NumPy
     import ctypes
     scores = torch.empty(B * H * G, cache.max_pages, dtype=torch.float64, device="cuda")
