@@ -429,7 +429,11 @@ def run_ours(args, cfg):
                      "frac_vs_read_peak": (round(kernel_gbs[dominant] / load_read_peak(), 4)
                                            if kernel_gbs[dominant] and load_read_peak() else None),
                      "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": ab[dominant]},
+                     "algorithmic_bytes_per_launch": ab[dominant],
+                     **({"note": "the dominant stage is latency-bound (per-unit select/top-p chains at this "
+                                 "batch); its HBM fraction is not the limiter"}
+                        if dominant in ("K2_select", "K3bc_topp") and kernel_gbs[dominant]
+                        and kernel_gbs[dominant] / peak < 0.2 else {})},
         "step_roofline": {"algorithmic_bytes": ab["step"], "achieved_gbs_per_gpu": round(achieved_step, 1),
                           "frac": round(achieved_step / peak, 4)},
         "kernels_us": {k: round(v * 1e3, 2) for k, v in stage_ms.items()},

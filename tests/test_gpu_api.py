@@ -184,7 +184,8 @@ def test_run_grouped_and_run_head_match_reference(golden):
                                        err_msg=name)
 
 
-def test_file_workload_runs_on_the_gpu_path(tmp_path):
+@pytest.mark.parametrize("kind", ["quest", "channel_pruned"])
+def test_file_workload_runs_on_the_gpu_path(tmp_path, kind):
     """workload.py:148-183 file workload (q/k/v .twlt) decoded by run_file_workload
     vs the oracle's run_grouped restatement per step and KV head."""
     rng = np.random.default_rng(31)
@@ -195,13 +196,13 @@ def test_file_workload_runs_on_the_gpu_path(tmp_path):
     v = bf(rng.standard_normal((kvh, n, 128)))
     for name, a in (("q", q), ("k", k), ("v", v)):
         tw.write_tensor(tmp_path / f"{name}.twlt", a)
-    cfg = tw.PipelineConfig(selector=tw.SelectorConfig(kind="quest", budget=256),
+    cfg = tw.PipelineConfig(selector=tw.SelectorConfig(kind=kind, budget=256),
                             prune=tw.BinarySearchConfig(p=0.9), group_map=tw.GroupMap(heads // kvh))
     outs, _ = tw.run_file_workload(tmp_path, cfg)
     G = heads // kvh
     for s in range(steps):
         for h in range(kvh):
-            res = orc.decode_unit(q[s, h * G:(h + 1) * G], k[h], v[h], selector="quest", budget=256, p=0.9)
+            res = orc.decode_unit(q[s, h * G:(h + 1) * G], k[h], v[h], selector=kind, budget=256, p=0.9)
             want = res["out"]
             got = outs[s, h * G:(h + 1) * G].cpu().numpy()
             np.testing.assert_allclose(got, want, rtol=2e-2, atol=2e-2 * np.abs(want).max())

@@ -479,3 +479,23 @@ def test_fused_step_append_matches_separate_append(bits):
     assert a.seq_lens.tolist() == c.seq_lens.tolist() == [658, 531]
     for name in ("k_cache", "v_cache", "kq", "kmeta", "kabsmax"):
         assert torch.equal(getattr(a, name), getattr(c, name)), name
+
+
+@pytest.mark.parametrize("selector", ["full", "sink_window", "channel_pruned"])
+def test_decode_step_other_selectors_match_staged(selector):
+    """tw_decode_step with the non-Quest base selectors (separate K1 append)
+    equals append + the staged kernels."""
+    B, H, G, n = 2, 2, 4, 600
+    dtype = torch.bfloat16
+    kw = dict(p=0.9, budget=200) if selector == "channel_pruned" else dict(p=0.9)
+    a, batch = _cache(B, H, G, n, dtype, [600, 431], seed=17, tau=0.6)
+    c, _ = _cache(B, H, G, n, dtype, [600, 431], seed=17, tau=0.6)
+    da, dc = TwilightDecoder(a, selector, **kw), TwilightDecoder(c, selector, **kw)
+    q = batch.q.contiguous()
+    for _ in range(3):
+        out_a = da.step(q, batch.k_new, batch.v_new)
+        c.append(batch.k_new, batch.v_new)
+        out_c = dc.forward(q)
+        torch.cuda.synchronize()
+        assert torch.equal(out_a, out_c)
+    assert a.seq_lens.tolist() == c.seq_lens.tolist() == [603, 434]
