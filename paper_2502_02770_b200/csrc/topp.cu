@@ -104,6 +104,37 @@ __device__ __forceinline__ double class_mass(double w, uint64_t cnt, uint64_t us
 __device__ __forceinline__ float4 ninf4() { return make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY); }
 __device__ __forceinline__ float comp(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
 
+// Inclusive scans of a (double, u32) pair per thread in one pass (two group barriers).
+__device__ __forceinline__ void grp_scan2(const Group& g, double v, uint32_t u, double* dtmp, uint32_t* utmp,
+                                          double& incl, uint32_t& uincl, double& total, uint32_t& utotal) {
+  const int lane = g.tid & 31, wid = g.warp(), nw = g.nwarps();
+  double x = v;
+  uint32_t y = u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double xs = __shfl_up_sync(0xffffffffu, x, o);
+    const uint32_t ys = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) { x += xs; y += ys; }
+  }
+  if (lane == 31) { dtmp[wid] = x; utmp[wid] = y; }
+  g.sync();
+  double pre = 0.0, tot = 0.0;
+  uint32_t upre = 0, utot = 0;
+  for (int i = 0; i < nw; ++i) {
+    const double sd = dtmp[i];
+    const uint32_t su = utmp[i];
+    pre += i < wid ? sd : 0.0;
+    tot += sd;
+    upre += i < wid ? su : 0u;
+    utot += su;
+  }
+  g.sync();
+  incl = x + pre;
+  uincl = y + upre;
+  total = tot;
+  utotal = utot;
+}
+
 template <typename T>
 __device__ __forceinline__ T grp_scan(const Group& g, T v, T* tmp, T& total) {
   const int lane = g.tid & 31, wid = g.warp(), nw = g.nwarps();
@@ -434,19 +465,24 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
       uint32_t b0;
       __shared__ double s_dtmp[GB][kGT / 32];
       __shared__ uint32_t s_utmp[GB][kGT / 32];
-      __shared__ int s_bin[GB];
-      __shared__ double s_above[GB];
-      __shared__ uint32_t s_acnt[GB];
 #ifndef TW_TT_SPLIT
       if (gp == 0) TT(6);
 #endif
-      const double incl = grp_scan<double>(grp, local, s_dtmp[gp], Z);
-      const uint32_t cincl = grp_scan<uint32_t>(grp, lc, s_utmp[gp], b0);
+      double incl;
+      uint32_t cincl;
+      grp_scan2(grp, local, lc, s_dtmp[gp], s_utmp[gp], incl, cincl, Z, b0);
       const double target = p_eff * Z;
-      if (grp.tid == 0) s_bin[gp] = -1;
+      HeadRec& r = R[g];
+      if (grp.tid == 0) {  // defaults: -1 = rounding left the target above the total -> keep everything
+        r.cb = -1;
+        r.Z = Z;
+        r.target = target;
+        r.b0 = b0;
+        r.zhi = r.zlo = -INFINITY;
+      }
       grp.sync();
       const double excl = incl - local;
-      if (excl < target && target <= incl) {
+      if (excl < target && target <= incl) {  // the one thread holding the crossing bin records it
         double run = excl;
         uint32_t crun = cincl - lc;
 #pragma unroll 1
@@ -454,35 +490,21 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
           uint32_t c;
           const double m = mass(i, c);
           if (c && run + m >= target) {
-            s_bin[gp] = bfirst + i;
-            s_above[gp] = run;
-            s_acnt[gp] = crun;
+            const int cb = bfirst + i;
+            r.cb = cb;
+            r.above_mass = run;
+            r.above_cnt = crun;
+            r.members = c;
+            r.wb = exp((double)bin_top(M, cb) - (double)M);
+            r.zhi = bin_ceiling(cb, M, M120);
+            r.zlo = bin_ceiling(cb + 1, M, M120);
             break;
           }
           run += m;
           crun += c;
         }
       }
-      grp.sync();
       if (gp == 0) TT(7);
-      if (grp.tid == 0) {
-        HeadRec& r = R[g];
-        const int cb = s_bin[gp];  // -1: rounding left the target above the total -> keep everything
-        r.cb = cb;
-        r.Z = Z;
-        r.target = target;
-        r.b0 = b0;
-        if (cb >= 0) {
-          r.above_mass = s_above[gp];
-          r.above_cnt = s_acnt[gp];
-          r.members = hc[cb];
-          r.wb = exp((double)bin_top(M, cb) - (double)M);
-          r.zhi = bin_ceiling(cb, M, M120);
-          r.zlo = bin_ceiling(cb + 1, M, M120);
-        } else {
-          r.zhi = r.zlo = -INFINITY;
-        }
-      }
     }
     __syncthreads();
   }
@@ -681,9 +703,9 @@ __global__ void __launch_bounds__(kHeadThreads) topp_head_kernel(tw_paged_kv kv,
   uint32_t* mpos = mkey + kHeadMC;
   __shared__ HeadRec R;
   __shared__ unsigned long long s_deep;
-  __shared__ int s_fill, s_last, s_first, s_bin;
-  __shared__ double s_dtmp[NW], s_above;
-  __shared__ uint32_t s_utmp[NW], s_acnt, s_wtot[NW];
+  __shared__ int s_fill, s_last, s_first;
+  __shared__ double s_dtmp[NW];
+  __shared__ uint32_t s_utmp[NW], s_wtot[NW];
   const int unit = blockIdx.x / G, g = blockIdx.x % G, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Group grp = whole_block();
   const size_t T = (size_t)kv.max_pages * kPage;
@@ -705,6 +727,7 @@ __global__ void __launch_bounds__(kHeadThreads) topp_head_kernel(tw_paged_kv kv,
     s_fill = 0;
     s_deep = 0;
   }
+  TT(0);
   if (!empty) {
     for (int i = tid; i < kBins; i += NT) Hc[i] = Hu[i] = 0;
     __syncthreads();
@@ -728,6 +751,7 @@ __global__ void __launch_bounds__(kHeadThreads) topp_head_kernel(tw_paged_kv kv,
     for (int o = 16; o > 0; o >>= 1) deep += __shfl_xor_sync(0xffffffffu, deep, o);
     if (lane == 0 && deep) atomicAdd(&s_deep, deep);
     __syncthreads();
+    TT(1);
     const int bfirst = tid * kPerT;
     const float t0 = bin_top(M, bfirst);
     const float w0 = (float)exp((double)t0 - (double)M);
@@ -750,13 +774,20 @@ __global__ void __launch_bounds__(kHeadThreads) topp_head_kernel(tw_paged_kv kv,
     }
     double Z;
     uint32_t b0;
-    const double incl = grp_scan<double>(grp, local, s_dtmp, Z);
-    const uint32_t cincl = grp_scan<uint32_t>(grp, lc, s_utmp, b0);
+    double incl;
+    uint32_t cincl;
+    grp_scan2(grp, local, lc, s_dtmp, s_utmp, incl, cincl, Z, b0);
     const double target = p_eff * Z;
-    if (tid == 0) s_bin = -1;
+    if (tid == 0) {  // defaults: -1 = rounding left the target above the total -> keep everything
+      R.cb = -1;
+      R.Z = Z;
+      R.target = target;
+      R.b0 = b0;
+      R.zhi = R.zlo = -INFINITY;
+    }
     __syncthreads();
     const double excl = incl - local;
-    if (excl < target && target <= incl) {
+    if (excl < target && target <= incl) {  // the one thread holding the crossing bin records it
       double run = excl;
       uint32_t crun = cincl - lc;
 #pragma unroll 1
@@ -764,37 +795,25 @@ __global__ void __launch_bounds__(kHeadThreads) topp_head_kernel(tw_paged_kv kv,
         uint32_t c;
         const double m = mass(i, c);
         if (c && run + m >= target) {
-          s_bin = bfirst + i;
-          s_above = run;
-          s_acnt = crun;
+          const int cb = bfirst + i;
+          R.cb = cb;
+          R.above_mass = run;
+          R.above_cnt = crun;
+          R.members = c;
+          R.wb = exp((double)bin_top(M, cb) - (double)M);
+          R.zhi = bin_ceiling(cb, M, M120);
+          R.zlo = bin_ceiling(cb + 1, M, M120);
+          if (c <= (uint32_t)kHeadMC) R.seg = 0;
+          else R.zlo = R.zhi;  // members re-read from the logits
           break;
         }
         run += m;
         crun += c;
       }
     }
-    __syncthreads();
-    if (tid == 0) {
-      const int cb = s_bin;
-      R.cb = cb;
-      R.Z = Z;
-      R.target = target;
-      R.b0 = b0;
-      if (cb >= 0) {
-        R.above_mass = s_above;
-        R.above_cnt = s_acnt;
-        R.members = Hc[cb];
-        R.wb = exp((double)bin_top(M, cb) - (double)M);
-        R.zhi = bin_ceiling(cb, M, M120);
-        R.zlo = bin_ceiling(cb + 1, M, M120);
-        if (R.members <= (uint32_t)kHeadMC) R.seg = 0;
-        else R.zlo = R.zhi;  // members re-read from the logits
-      } else {
-        R.zhi = R.zlo = -INFINITY;
-      }
-    }
   }
   __syncthreads();
+  TT(2);
   // ---- pass 2 (this head): kept positions ORed into the unit bitmap, crossing-bin members listed
   {
     const float zhi = R.zhi, zlo = R.zlo;
@@ -821,6 +840,7 @@ __global__ void __launch_bounds__(kHeadThreads) topp_head_kernel(tw_paged_kv kv,
     }
   }
   __syncthreads();
+  TT(3);
   // ---- resolve the threshold class of this head
   {
     const HeadRec& h = R;
@@ -868,12 +888,14 @@ __global__ void __launch_bounds__(kHeadThreads) topp_head_kernel(tw_paged_kv kv,
       stats[3] = (float)h.b0;
     }
   }
+  TT(4);
   // ---- the unit's last head CTA compacts the union
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(buf.topp_done + unit, 1) == G - 1;
   __syncthreads();
   if (!s_last) return;
+  TT(5);
   __threadfence();
   const int* cand = buf.cand_pages + (size_t)unit * kv.max_pages;
   int* out = buf.final_idx + (size_t)unit * T;
@@ -890,6 +912,13 @@ __global__ void __launch_bounds__(kHeadThreads) topp_head_kernel(tw_paged_kv kv,
   for (int i = 0; i < NW; ++i) {
     run += i < warp ? s_wtot[i] : 0u;
     basei += s_wtot[i];
+  }
+  // claim the unit's attention work items now: the atomic's latency overlaps the emission
+  const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : TW_DEFAULT_CHUNK;
+  const int nitems = ((int)basei + chunk - 1) / chunk;
+  if (tid == 0) {
+    buf.final_count[unit] = (int)basei;
+    s_first = nitems ? (int)atomicAdd(&buf.counters[0], (uint32_t)nitems) : 0;
   }
   for (int w0 = wlo; w0 < whi; w0 += 32) {
     const int w = w0 + lane;
@@ -915,16 +944,13 @@ __global__ void __launch_bounds__(kHeadThreads) topp_head_kernel(tw_paged_kv kv,
     }
     run += __shfl_sync(0xffffffffu, incl, 31);
   }
-  const int chunk = prm.chunk_tokens > 0 ? prm.chunk_tokens : TW_DEFAULT_CHUNK;
-  const int nitems = ((int)basei + chunk - 1) / chunk;
+  __syncthreads();
+  TT(6);
   if (tid == 0) {
-    buf.final_count[unit] = (int)basei;
-    s_first = nitems ? (int)atomicAdd(&buf.counters[0], (uint32_t)nitems) : 0;
     buf.unit_items[2 * unit] = s_first;
     buf.unit_items[2 * unit + 1] = nitems;
     buf.topp_done[unit] = 0;
   }
-  __syncthreads();
   for (int i = tid; i < nitems; i += NT) {
     if (s_first + i < buf.max_items) {
       buf.work_items[2 * (s_first + i)] = unit;

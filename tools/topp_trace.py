@@ -41,10 +41,16 @@ for rep in range(3):
     _lib.lib().tw_debug_ttrace(buf)
 a = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8).astype(np.int64)
 rows = a[a[:, 0] > 0]
-nph = int((rows > 0).sum(axis=1).max())
 t0 = rows[:, 0].min()
+print(f"ctas={len(rows)} span={(rows.max() - t0) / 1e3:.2f}us start_spread={(rows[:, 0].max() - t0) / 1e3:.2f}us")
+full = rows[(rows > 0).all(axis=1)] if (rows > 0).all(axis=1).any() else None
+nph = int((rows > 0).sum(axis=1).min())  # phases every CTA records
 order = np.argsort(rows[0, :nph])
-print("slot order", order.tolist())
 d = np.diff(rows[:, :nph][:, order], axis=1) / 1e3
-print(f"ctas={len(rows)} span={(rows[:, nph - 1].max() - t0) / 1e3:.2f}us start_spread={(rows[:, 0].max() - t0) / 1e3:.2f}us")
-print("phase means us:", d.mean(axis=0).round(2).tolist(), " max:", d.max(axis=0).round(2).tolist())
+print("slot order", order.tolist())
+print("phase means us (all CTAs):", d.mean(axis=0).round(2).tolist(), " max:", d.max(axis=0).round(2).tolist())
+nfull = int((rows > 0).sum(axis=1).max())
+if nfull > nph:
+    last = rows[(rows > 0).sum(axis=1) == nfull][:, :nfull]
+    dl = np.diff(np.sort(last, axis=1), axis=1) / 1e3
+    print("CTAs with all phases:", len(last), "phase means us:", dl.mean(axis=0).round(2).tolist())
