@@ -51,7 +51,7 @@ constexpr int kFilterPagesPerCta = TW_QF_ITEM;  // largest filter item (<= 64: t
 
 // ---------------------------------------------------------------- filter pass
 
-// Persistent warp workers over (unit, 64-page) items, chunk-major.  Each warp
+// Persistent warp workers over (unit, 16..64-page) items, chunk-major.  Each warp
 // streams its pages' metadata (lo|hi, 512 B in bf16) through a 4-stage
 // cp.async ring of 2-page stages; a half-warp scores one page (16 lanes x 8
 // channels) for all G heads and reduces with shuffles.
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_kernel(tw_paged_kv
 //   score = qneg . lo + qpos . hi,  qpos = max(q, 0), qneg = min(q, 0),
 // i.e. a [pages x 256] x [256 x heads] product -> legacy mma.sync m16n8k16
 // (bf16 products exact, fp32 accumulation, covered by the select margin).
-// Per warp: 16-page tiles (16 x 512 B, XOR-swizzled rows) through a 3-stage
+// Per warp: 16-page tiles (16 x 512 B, XOR-swizzled rows) through a TW_QM_STAGES-deep (2)
 // cp.async ring; one ldmatrix.x4 + one MMA per page-tile k-step.
 #ifndef TW_QM_STAGES
 #define TW_QM_STAGES 2
