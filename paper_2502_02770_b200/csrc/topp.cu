@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
         m120[h] = Mh[h] * kBinPerLogit;
         deep[h] = 0;
       }
-#pragma unroll 2
+#pragma unroll (G >= 4 ? 4 : 2)  // logit-pass unrolling, measured per G (C2/C5 vs C3)
       for (int i = tid; i < n4; i += NT) {
         float4 v[GB];
 #pragma unroll
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(UnitCfg<G, HB>::NT) topp_unit_kernel(tw_paged_
     int sg[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) { zhi[g] = R[g].zhi; zlo[g] = R[g].zlo; sg[g] = R[g].seg; }
-#pragma unroll 2
+#pragma unroll (G >= 4 ? 1 : 2)
     for (int i0 = 0; i0 < n4; i0 += NT) {
       const int i = i0 + tid;
       const bool valid = i < n4;
