@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(1024) append_kernel(tw_paged_kv kv, const T* _
   const int pos = positions[b];
   append_row_warp<T, BITS>(kv, b, h, lane, k_new, v_new, pos);
   __syncthreads();
-  if (threadIdx.x == 0) kv.seq_lens[b] = pos + 1;
+  if (threadIdx.x == 0 && pos >= 0 && pos < kv.max_pages * kPage) kv.seq_lens[b] = pos + 1;
 }
 
 // Bulk build: block (logical page, sequence), one warp per kv head walking the

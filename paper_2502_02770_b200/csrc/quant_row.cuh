@@ -88,11 +88,13 @@ __device__ __forceinline__ void write_quant(uint8_t* qblock, int slot, int lane,
 
 // Append the row at `pos` of (sequence b, kv head h): bf16/fp32 K and V into
 // the paged pool, b-bit codes + params, the open page's channel min/max, and
-// the |k| bound.  One warp; lane l owns channels 4l..4l+3.
+// the |k| bound.  One warp; lane l owns channels 4l..4l+3.  A position beyond
+// the page table's capacity is dropped (no out-of-bounds write).
 template <typename T, int BITS>
 __device__ __forceinline__ void append_row_warp(const tw_paged_kv& kv, int b, int h, int lane, const T* k_new,
                                                 const T* v_new, int pos) {
   const int H = kv.num_kv_heads;
+  if (pos < 0 || pos >= kv.max_pages * kPage) return;  // outside the sequence's page table: dropped
   const int logical = pos / kPage, slot = pos % kPage;
   const int phys = kv.page_table[(size_t)b * kv.max_pages + logical];
   const size_t ph = (size_t)phys * H + h;

@@ -190,17 +190,19 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
     const int unit = it % units;
     const int p0 = (it / units) * item;
     const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
-    const int n = positions ? __ldg(positions + b) + 1 : kv.seq_lens[b];
+    const int pos = positions ? __ldg(positions + b) : -1;
+    const int n = positions ? min(pos + 1, kv.max_pages * kPage) : kv.seq_lens[b];
     const int npages = (n + kPage - 1) / kPage;
     if (p0 >= npages) continue;
     const int np = min(item, npages - p0);
     if (positions && npages - 1 < p0 + np) {  // this item holds the open page: append first
       switch (kv.bits) {
-        case 2: append_row_warp<__nv_bfloat16, 2>(kv, b, h, lane, k_new, v_new, n - 1); break;
-        case 8: append_row_warp<__nv_bfloat16, 8>(kv, b, h, lane, k_new, v_new, n - 1); break;
-        default: append_row_warp<__nv_bfloat16, 4>(kv, b, h, lane, k_new, v_new, n - 1); break;
+        case 2: append_row_warp<__nv_bfloat16, 2>(kv, b, h, lane, k_new, v_new, pos); break;
+        case 8: append_row_warp<__nv_bfloat16, 8>(kv, b, h, lane, k_new, v_new, pos); break;
+        default: append_row_warp<__nv_bfloat16, 4>(kv, b, h, lane, k_new, v_new, pos); break;
       }
-      if (h == 0 && lane == 0) kv.seq_lens[b] = n;  // every reader in this kernel uses positions
+      if (h == 0 && lane == 0 && pos < kv.max_pages * kPage)
+        kv.seq_lens[b] = n;  // every reader in this kernel uses positions
       __threadfence();  // the metadata stores precede this warp's cp.async reads of the page
       __syncwarp();
     }

@@ -499,3 +499,27 @@ def test_decode_step_other_selectors_match_staged(selector):
         torch.cuda.synchronize()
         assert torch.equal(out_a, out_c)
     assert a.seq_lens.tolist() == c.seq_lens.tolist() == [603, 434]
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_append_beyond_capacity_is_dropped(fused):
+    """A position past the sequence's page table is dropped by K1 (separate
+    append kernel and the append fused into the Quest filter): no write, the
+    length unchanged; the other sequences append normally."""
+    B, H, G = 2, 2, 4
+    P = 8
+    dtype = torch.bfloat16
+    batch = make_batch(B, H, G, P * 16, dtype, seed=91)
+    cache = PagedKVCache(B, H, G, max_pages=P, dtype=dtype)
+    cache.prefill(batch.K, batch.V, [P * 16, 100])
+    before = [t.clone() for t in (cache.k_cache, cache.v_cache, cache.kq, cache.kmeta)]
+    pos = torch.tensor([P * 16, 100], dtype=torch.int32, device="cuda")
+    if fused:
+        TwilightDecoder(cache, "quest", budget=32, p=0.9).step(batch.q.contiguous(), batch.k_new, batch.v_new, pos)
+    else:
+        cache.append(batch.k_new, batch.v_new, pos)
+    torch.cuda.synchronize()
+    assert cache.seq_lens.tolist() == [P * 16, 101]
+    for t0, t1 in zip(before, (cache.k_cache, cache.v_cache, cache.kq, cache.kmeta)):
+        assert torch.equal(t0[:P], t1[:P])  # sequence 0 owns physical pages 0..P-1
+    assert torch.equal(cache.unit_keys(1, 0)[100], batch.k_new[1, 0])
