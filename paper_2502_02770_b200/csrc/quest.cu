@@ -428,8 +428,21 @@ __global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv k
         if (lane == 0) { gs.margin = qa * amax * (300.0f / 16777216.0f); gs.namb = 0; gs.cin = 0; }
       }
       for (int i = grp.tid; i < words; i += grp.nthreads) hbits[i] = 0;
+      if ((Pmax & 3) == 0) {  // rows 16-byte aligned: four scores per load, all in flight at once
+        const int P4 = P >> 2;
+#pragma unroll 4
+        for (int i = grp.tid; i < P4; i += grp.nthreads) {
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(sc) + i);
+          keys[4 * i] = f2key(v.x);
+          keys[4 * i + 1] = f2key(v.y);
+          keys[4 * i + 2] = f2key(v.z);
+          keys[4 * i + 3] = f2key(v.w);
+        }
+        for (int i = 4 * P4 + grp.tid; i < P; i += grp.nthreads) keys[i] = f2key(__ldcg(sc + i));
+      } else {
 #pragma unroll 8
-      for (int i = grp.tid; i < P; i += grp.nthreads) keys[i] = f2key(__ldcg(sc + i));
+        for (int i = grp.tid; i < P; i += grp.nthreads) keys[i] = f2key(__ldcg(sc + i));
+      }
       grp.sync();
       STRACE();
       const float t = key2f(group_kth_largest_lin(grp, keys, P, (uint32_t)k, hist, gs.mem, gs.tmp, gs.res));
