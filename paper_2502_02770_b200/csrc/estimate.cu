@@ -436,10 +436,10 @@ static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, estimate_kernel<T, G, BITS>, kEstWarps * 32, 0);
   int grid = sms * persist_cap(per_sm);
   // item size: 32 pages (amortises the per-item index lookups and ring fill) unless
-  // that leaves warps idle -- small batches split into 16- or 8-page items
+  // that leaves warps idle -- small batches split into 16-, 8- or 4-page items
   const int units = kv->num_seqs * kv->num_kv_heads;
   int item = kEstPagesPerCta;
-  while (item > 8 && (long long)units * ((kv->max_pages + item - 1) / item) < (long long)grid * kEstWarps) item /= 2;
+  while (item > 4 && (long long)units * ((kv->max_pages + item - 1) / item) < (long long)grid * kEstWarps) item /= 2;
   const int max_chunks = (kv->max_pages + item - 1) / item;
   const int items = units * max_chunks;
   if (grid * kEstWarps > items) grid = (items + kEstWarps - 1) / kEstWarps;
