@@ -6,12 +6,17 @@ extern "C" int32_t tw_version(void) { return 100; }  // 0.1.0
 int tw_select_append(const tw_paged_kv* kv, const void* q, const void* k_new, const void* v_new,
                      const int32_t* positions, const tw_decode_params* prm, const tw_decode_buffers* buf,
                      cudaStream_t stream);  // quest.cu
+int tw_attn_geometry(const tw_paged_kv* kv, int chunk);  // attention.cu
 
 extern "C" int tw_decode_step(const tw_paged_kv* kv, const void* q, const void* k_new, const void* v_new,
                               const int32_t* positions, const tw_decode_params* prm,
                               const tw_decode_buffers* buf, float* out, cudaStream_t stream) {
+  if (!kv || !prm || !buf || !out) return TW_ERR_INVALID;
+  // reject a bad attention geometry before K1 appends and advances seq_lens
+  if (int s = tw_attn_geometry(kv, prm->chunk_tokens > 0 ? prm->chunk_tokens : TW_DEFAULT_CHUNK)) return s;
+  if (prm->renormalize != 1) return TW_ERR_INVALID;
   int s = tw_select_append(kv, q, k_new, v_new, positions, prm, buf, stream);  // K1 fused into the Quest filter
-  if (s == 1) {
+  if (s == tw::TW_FUSE_UNAVAILABLE) {
     if ((s = tw_quant_append(kv, k_new, v_new, positions, stream))) return s;
     s = tw_select(kv, q, prm, buf, stream);
   }

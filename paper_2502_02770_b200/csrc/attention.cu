@@ -505,6 +505,17 @@ __global__ void __launch_bounds__(kHeadDim) merge_kernel(tw_paged_kv kv, tw_deco
 
 using namespace tw;
 
+// Work-item geometry the attention + merge kernels accept: chunks of whole
+// 16-row tiles, at most kMaxChunk tokens, and at most 1024 items per unit (the
+// merge kernel's per-(unit, head) weights).  Checked by tw_decode_step before
+// K1 mutates the cache.
+int tw_attn_geometry(const tw_paged_kv* kv, int chunk) {
+  if (chunk < kTile || chunk > kMaxChunk || chunk % kTile != 0) return TW_ERR_INVALID;
+  const int64_t T_tokens = (int64_t)kv->max_pages * kPage;
+  if ((T_tokens + chunk - 1) / chunk > 1024) return TW_ERR_INVALID;
+  return TW_OK;
+}
+
 template <typename T, int G, bool DENSE>
 static int launch_attn(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, float* out, int chunk,
                        cudaStream_t s) {
@@ -512,9 +523,7 @@ static int launch_attn(const tw_paged_kv* kv, const T* q, const tw_decode_buffer
   const int T_tokens = kv->max_pages * kPage;
   const int max_chunks = (T_tokens + chunk - 1) / chunk;
   const int total = DENSE ? units * max_chunks : (int)buf->max_items;
-  if (chunk > kMaxChunk || chunk % kTile != 0) return TW_ERR_INVALID;
-  if (max_chunks > 1024) return TW_ERR_INVALID;  // items of one unit fit the merge kernel's weights
-  if ((int64_t)max_chunks * G > 2048) return TW_ERR_INVALID;  // merge weights fit shared memory
+  if (int st = tw_attn_geometry(kv, chunk)) return st;
   if (DENSE && (int64_t)units * max_chunks > buf->max_items) return TW_ERR_INVALID;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

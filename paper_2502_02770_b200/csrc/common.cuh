@@ -127,6 +127,10 @@ __device__ __forceinline__ float exp_diff(float z, float m) {
 
 // ---------------------------------------------------------------- launch check
 
+// Internal (not a tw_status): the fused K1+K2 launch does not apply, nothing
+// was enqueued, and the caller runs the separate append + select.
+constexpr int TW_FUSE_UNAVAILABLE = -1;
+
 inline int launch_status() {
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TW_OK : TW_ERR_CUDA;

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
                                                                          uint32_t* __restrict__ ctr, int item,
                                                                          const __nv_bfloat16* __restrict__ k_new,
                                                                          const __nv_bfloat16* __restrict__ v_new,
-                                                                         const int32_t* __restrict__ positions) {
+                                                                         const int32_t* positions) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(128) uint8_t qm_ring[];
@@ -541,6 +541,8 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
                          const tw_decode_buffers* buf, cudaStream_t stream, const void* k_new = nullptr,
                          const void* v_new = nullptr, const int32_t* positions = nullptr) {
   const int units = kv->num_seqs * kv->num_kv_heads;
+  const size_t smem = select_smem_bytes(kv->max_pages);
+  if (smem > 227 * 1024) return TW_ERR_INVALID;  // checked before anything is enqueued
   cudaMemsetAsync(buf->counters, 0, 8 * sizeof(uint32_t), stream);
   if (prm->selector == TW_SELECT_QUEST) {
     int dev = 0, sms = 148;
@@ -589,8 +591,6 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
       }
     }
   }
-  const size_t smem = select_smem_bytes(kv->max_pages);
-  if (smem > 227 * 1024) return TW_ERR_INVALID;
   cudaFuncSetAttribute(quest_select_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   launch_pdl(quest_select_kernel<T>, dim3(units), dim3(kSelThreads), smem, stream, *kv, (const T*)q, *prm, *buf);
   return launch_status();
@@ -600,8 +600,10 @@ int tw_select_channel_pruned(const tw_paged_kv* kv, const void* q, const tw_deco
                              const tw_decode_buffers* buf, cudaStream_t stream);  // channel.cu
 
 // The decode step's K1 + K2 in one pass when the Quest filter runs on the bf16
-// tensor-core kernel: returns 1 (nothing launched) when the step must append
-// separately (fp32 cache, other selectors, all-pages budget).
+// tensor-core kernel.  Returns TW_FUSE_UNAVAILABLE (nothing launched) when the
+// step must append separately: fp32 cache, other selectors, a select kernel
+// that would not fit shared memory, or `positions` aliasing kv->seq_lens (the
+// filter writes seq_lens while later items still read their positions).
 int tw_select_append(const tw_paged_kv* kv, const void* q, const void* k_new, const void* v_new,
                      const int32_t* positions, const tw_decode_params* prm, const tw_decode_buffers* buf,
                      cudaStream_t stream) {
@@ -611,8 +613,9 @@ int tw_select_append(const tw_paged_kv* kv, const void* q, const void* k_new, co
       (kv->group_size != 1 && kv->group_size != 2 && kv->group_size != 4 && kv->group_size != 8) ||
       (kv->bits != 0 && kv->bits != 2 && kv->bits != 4 && kv->bits != 8) || prm->budget_pages < 1 ||
       !buf->page_scores || !buf->band_idx || !buf->band_scores || !q || !buf->cand_pages || !buf->cand_count ||
-      !buf->counters || !buf->head_max)
-    return 1;
+      !buf->counters || !buf->head_max || positions == kv->seq_lens ||
+      select_smem_bytes(kv->max_pages) > 227 * 1024)
+    return TW_FUSE_UNAVAILABLE;
   return launch_select<__nv_bfloat16>(kv, q, prm, buf, stream, k_new, v_new, positions);
 }
 

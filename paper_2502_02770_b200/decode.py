@@ -171,19 +171,46 @@ class DecodeStats:
     cand_pages: torch.Tensor  # union pages per unit
 
 
+MAX_CHUNK = 512        # tokens per attention work item (csrc/attention.cu kMaxChunk)
+MAX_UNIT_ITEMS = 1024  # work items of one unit the split-KV merge accepts
+
+
+def min_chunk(max_pages: int) -> int:
+    """Smallest work-item size (multiple of 16) that splits a full context
+    of max_pages pages into at most MAX_UNIT_ITEMS items."""
+    T = max_pages * L.PAGE_SIZE
+    return max(L.PAGE_SIZE, 16 * -(-(-(-T // MAX_UNIT_ITEMS)) // 16))
+
+
+def check_chunk(chunk: int, max_pages: int) -> int:
+    """tw_attn_geometry on the host: raise ValueError before any kernel runs."""
+    chunk = int(chunk)
+    if chunk % L.PAGE_SIZE or not L.PAGE_SIZE <= chunk <= MAX_CHUNK:
+        raise ValueError(f"chunk_tokens {chunk} must be a multiple of 16 in [16, {MAX_CHUNK}]")
+    if chunk < min_chunk(max_pages):
+        raise ValueError(f"chunk_tokens {chunk} splits a {max_pages}-page context into more than "
+                         f"{MAX_UNIT_ITEMS} work items (need >= {min_chunk(max_pages)})")
+    return chunk
+
+
 def auto_chunk(cache: "PagedKVCache", sms: int = 148, warps_per_sm: int = 8) -> int:
     """Attention work-item size: ~4 items per worker warp when half the
-    context survives, clamped to [64, 512] tokens (multiple of 16)."""
+    context survives, clamped to [64, 512] tokens (multiple of 16) and never
+    below min_chunk (at most 1024 items per unit for the merge)."""
     units = cache.num_seqs * cache.num_kv_heads
     est = units * cache.max_pages * L.PAGE_SIZE * 0.5 / (4 * sms * warps_per_sm)
-    return 512 if est >= 384 else int(max(64, 16 * round(est / 16)))
+    c = 512 if est >= 384 else int(max(64, 16 * round(est / 16)))
+    c = max(c, min_chunk(cache.max_pages))
+    if c > MAX_CHUNK:
+        raise ValueError(f"context of {cache.max_pages} pages exceeds {MAX_UNIT_ITEMS} x {MAX_CHUNK} tokens")
+    return c
 
 
 class DecodeBuffers:
     """Caller-owned intermediate buffers of one decode step (tw_decode_buffers)."""
 
     def __init__(self, cache: PagedKVCache, chunk_tokens: int | None = None, head_page_bits: bool = False):
-        chunk_tokens = chunk_tokens or auto_chunk(cache)
+        chunk_tokens = check_chunk(chunk_tokens, cache.max_pages) if chunk_tokens else auto_chunk(cache)
         dev = cache.device
         U = cache.num_seqs * cache.num_kv_heads
         Hq = U * cache.group_size
@@ -263,7 +290,7 @@ class TwilightDecoder:
             self.params = self.waves[0][2].params
             self.bufs = [wv[2].bufs for wv in self.waves]
             return
-        chunk_tokens = chunk_tokens or auto_chunk(cache)
+        chunk_tokens = check_chunk(chunk_tokens, cache.max_pages) if chunk_tokens else auto_chunk(cache)
         if selector not in ("quest", "full", "sink_window", "channel_pruned"):
             raise ValueError(f"selector {selector!r} is not on the accelerated path "
                              "(quest | full | sink_window | channel_pruned)")

@@ -13,7 +13,7 @@ import pytest
 import torch
 
 from oracle import twilight_oracle as orc
-from tests.gpu_util import f2key_np, to_np, topp_set_ok
+from tests.gpu_util import check_unit_topp, f2key_np, to_np, topp_set_ok
 
 pytestmark = pytest.mark.gpu
 
@@ -314,15 +314,11 @@ def test_sink_window_selector_batched(dtype, sink, window):
             valid = np.isfinite(z_all[0])
             np.testing.assert_array_equal(pos[valid], want_cand)
             Qn = to_np(q[b, h * G:(h + 1) * G])
-            res = orc.decode_unit(Qn, K, V, selector="sink_window", p=p, sink=sink, window=window,
-                                  logits_override=[z_all[g][valid] for g in range(G)])
-            final = bufs.final_idx[u, : int(bufs.final_count[u])].cpu().numpy()
+            _, _, _, final, _ = check_unit_topp(bufs, u, G, p)
             assert np.isin(final, want_cand).all()
-            if not np.array_equal(final, res["final"]):
-                assert np.setxor1d(final, res["final"]).size <= 2  # threshold ties only
-                continue
             for g in range(G):
-                want = res["out"][g]
+                w = orc.full_weights(Qn[g], K)
+                want = orc.subset_attention(w, V, final, True)
                 np.testing.assert_allclose(to_np(out[b, h * G + g]), want, rtol=1e-4, atol=1e-4 * np.abs(want).max())
 
 
@@ -410,15 +406,11 @@ def test_channel_pruned_selector_batched(dtype, top_channels, budget):
             if not np.array_equal(got, want_cand):
                 assert all(_near_tie_ok(got, want_cand, Qn[g], K, ids, budget) for g in range(G))
                 continue
-            res = orc.decode_unit(Qn, K, V, selector="channel_pruned", budget=budget, p=p, top_channels=count,
-                                  logits_override=[z_all[g][valid] for g in range(G)])
-            final = bufs.final_idx[u, : int(bufs.final_count[u])].cpu().numpy()
+            _, _, _, final, _ = check_unit_topp(bufs, u, G, p)
             assert np.isin(final, want_cand).all()
-            if not np.array_equal(final, res["final"]):
-                assert np.setxor1d(final, res["final"]).size <= 2  # threshold ties only
-                continue
             for g in range(G):
-                want = res["out"][g]
+                w = orc.full_weights(Qn[g], K)
+                want = orc.subset_attention(w, V, final, True)
                 np.testing.assert_allclose(to_np(out[b, h * G + g]), want, rtol=1e-4, atol=1e-4 * np.abs(want).max())
 
 
@@ -523,3 +515,47 @@ def test_append_beyond_capacity_is_dropped(fused):
     for t0, t1 in zip(before, (cache.k_cache, cache.v_cache, cache.kq, cache.kmeta)):
         assert torch.equal(t0[:P], t1[:P])  # sequence 0 owns physical pages 0..P-1
     assert torch.equal(cache.unit_keys(1, 0)[100], batch.k_new[1, 0])
+
+
+def test_step_with_default_positions_many_waves():
+    """step() without positions passes cache.seq_lens as the append positions.
+    The fused K1+K2 filter writes seq_lens while later filter items still read
+    their positions, so the aliased case must take the separate append (ADVICE
+    r01): many filter items per unit (B*H well above the SM count) and every
+    length a multiple of 16 * 64 tokens (the open page starts a new item)."""
+    B, H, G, n = 40, 8, 4, 2048
+    dtype = torch.bfloat16
+    a, batch = _cache(B, H, G, n, dtype, [n] * B, seed=23, tau=0.6, extra_pages=2)
+    c, _ = _cache(B, H, G, n, dtype, [n] * B, seed=23, tau=0.6, extra_pages=2)
+    q = batch.q.contiguous()
+    da = TwilightDecoder(a, "quest", budget=512, p=0.9)
+    dc = TwilightDecoder(c, "quest", budget=512, p=0.9)
+    for _ in range(2):
+        out_a = da.step(q, batch.k_new, batch.v_new)  # positions = seq_lens (aliased)
+        c.append(batch.k_new, batch.v_new)
+        out_c = dc.forward(q)
+        torch.cuda.synchronize()
+        assert torch.equal(out_a, out_c)
+    assert a.seq_lens.tolist() == c.seq_lens.tolist() == [n + 2] * B
+    for name in ("k_cache", "v_cache", "kq", "kmeta", "kabsmax"):
+        assert torch.equal(getattr(a, name), getattr(c, name)), name
+
+
+def test_chunk_geometry_validated_before_any_kernel():
+    """A work-item size the merge cannot take is rejected on the host (and by
+    tw_decode_step before K1 appends); auto_chunk never picks one."""
+    from paper_2502_02770_b200.decode import auto_chunk, min_chunk
+    B, H, G = 1, 8, 4
+    cache = PagedKVCache(B, H, G, max_pages=2049, dtype=torch.bfloat16)  # 32k context + one spare page
+    assert auto_chunk(cache) >= min_chunk(2049) and auto_chunk(cache) % 16 == 0
+    TwilightDecoder(cache, "quest", budget=8192, p=0.95)  # builds: the old 513 * 4 > 2048 limit is gone
+    big = PagedKVCache(1, 1, 1, max_pages=8192, dtype=torch.bfloat16)
+    with pytest.raises(ValueError):
+        TwilightDecoder(big, "full", p=0.9, chunk_tokens=64)  # 2048 items per unit
+    dec = TwilightDecoder(big, "full", p=0.9)
+    dec.params.chunk_tokens = 64  # bypass the host check: the C ABI rejects it before appending
+    k = torch.zeros(1, 1, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):
+        dec.step(torch.zeros(1, 1, 128, dtype=torch.bfloat16, device="cuda"), k, k)
+    torch.cuda.synchronize()
+    assert big.seq_lens.tolist() == [0]
