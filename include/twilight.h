@@ -60,6 +60,11 @@ typedef enum {
   TW_SELECT_CHANNEL_PRUNED = 3
 } tw_selector;
 
+typedef enum {
+  TW_ESTIMATE_INT = 0,   /* INT-b key cache, PagedKVCache.bits */
+  TW_ESTIMATE_EXACT = 1  /* K[idx] @ q / sqrt(d) from k_cache */
+} tw_estimator;
+
 typedef struct tw_paged_kv {
   int32_t num_seqs;       /* B */
   int32_t num_kv_heads;   /* H_kv */
@@ -92,6 +97,8 @@ typedef struct tw_decode_params {
   int32_t channels_fixed;/* channel-pruned selector: 0 = rank the channels by mean |K| and write them to
                            chan_ids; 1 = use the top_channels ids already in chan_ids (the slice fixed
                            once per context, selectors.py:203) */
+  int32_t estimator;    /* tw_estimator: the cache's INT codes (estimate_scores, quantcache.py:238-272) or
+                           the full-precision keys (estimator_bits="exact", pipeline.py:212-214) */
 } tw_decode_params;
 
 /* Intermediate buffers of one decode step (all caller-allocated, sizes in
@@ -158,7 +165,9 @@ int tw_select(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
               const tw_decode_buffers* buf, cudaStream_t stream);
 
 /* K3a -- INT4 estimate over the candidate pages for all G heads of a unit:
- * estimate_scores (quantcache.py:238-272) as called at pipeline.py:342. */
+ * estimate_scores (quantcache.py:238-272) as called at pipeline.py:342; with
+ * prm->estimator == TW_ESTIMATE_EXACT the logits come from the full-precision
+ * keys instead (_candidate_logits exact path, pipeline.py:212-214). */
 int tw_estimate(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
                 const tw_decode_buffers* buf, cudaStream_t stream);
 

@@ -315,8 +315,58 @@ def main() -> None:
         ch[f"p{i}/cfg"] = np.array([budget, p, 1.0 if isinstance(budget, float) else 0.0, -1 if top is None else top])
         ch[f"p{i}/out"], ch[f"p{i}/final"], ch[f"p{i}/b0"] = np.asarray(outs), finals[0], np.array(b0)
     np.savez_compressed(os.path.join(OUT, "channel.npz"), **ch)
+    rows_and_exact()
     print("golden vectors written to", OUT)
 
 
+def rows_and_exact() -> None:
+    """rows.npz: dequantize_row / unpack_codes answers (quantcache.py:117-160)
+    and run_grouped / run_head with the exact estimator -- bypass_config
+    (pipeline.py:129-136) and estimator_bits="exact" under Quest -- as the
+    reference computes them (pipeline.py:204-216)."""
+    sys.path.insert(0, REF)
+    import nucleuskv as nk
+
+    rng = np.random.default_rng(20251017)
+    out = {}
+    for r in range(6):
+        bits = (2, 4, 8)[r % 3]
+        k = rng.standard_normal(128).astype(np.float32) * (1 + r)
+        codes, prm = nk.quantize_row(k, bits=bits)
+        out[f"deq{r}/codes"], out[f"deq{r}/params"] = codes, np.array([prm.scale, prm.zero])
+        out[f"deq{r}/f64"] = nk.dequantize_row(codes, prm)
+        out[f"deq{r}/f32"] = nk.dequantize_row(codes, prm, dtype=np.float32)
+    for r in range(4):
+        packed = rng.integers(0, 256, size=64 if r else 8, dtype=np.uint8)
+        out[f"unpack{r}/packed"] = packed
+        out[f"unpack{r}/codes"] = nk.unpack_codes(packed.tobytes(), 2 * packed.size)
+    for i, (n, G, kind, budget, p, dt) in enumerate([(700, 4, "full", None, 1.0, "f32"), (513, 1, "full", None, 1.0, "f32"),
+                                                     (900, 4, "quest", 256, 0.9, "f32"),
+                                                     (640, 2, "quest", 0.3, 0.95, "bf16")]):
+        K = rng.standard_normal((n, 128)).astype(np.float32)
+        V = rng.standard_normal((n, 128)).astype(np.float32)
+        Q = (rng.standard_normal((G, 128)) * 1.5).astype(np.float32)
+        if dt == "bf16":
+            K, V, Q = bf16_round(K), bf16_round(V), bf16_round(Q)
+        base = nk.PipelineConfig(selector=nk.SelectorConfig(kind=kind, budget=budget),
+                                 prune=nk.BinarySearchConfig(p=p), group_map=nk.GroupMap(G))
+        cfg = nk.bypass_config(base) if kind == "full" else \
+            nk.PipelineConfig(selector=base.selector, prune=base.prune, group_map=base.group_map, estimator_bits="exact")
+        if G == 1:
+            o, oc, rep = nk.run_head(Q[0], K, V, cfg)
+            outs, finals, b0 = np.asarray(o)[None], oc.selection.indices, rep.b0
+        else:
+            o, ocs, reps = nk.run_grouped(Q, K, V, cfg)
+            outs, finals, b0 = np.asarray(o), ocs[0].selection.indices, reps[0].b0
+        out[f"x{i}/K"], out[f"x{i}/V"], out[f"x{i}/Q"] = K, V, Q
+        out[f"x{i}/cfg"] = np.array([-1 if budget is None else budget, p, 1.0 if isinstance(budget, float) else 0.0,
+                                     1.0 if kind == "quest" else 0.0])
+        out[f"x{i}/out"], out[f"x{i}/final"], out[f"x{i}/b0"] = outs, np.asarray(finals), np.array([b0])
+    np.savez_compressed(os.path.join(OUT, "rows.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    if "--rows" in sys.argv:
+        rows_and_exact()
+    else:
+        main()

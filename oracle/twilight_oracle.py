@@ -262,6 +262,19 @@ def estimate_logits(q, codes, scale, zero, token_idx) -> np.ndarray:
     return (k_hat.astype(qv.dtype) @ qv) * inv
 
 
+def exact_logits(q, K, token_idx) -> np.ndarray:
+    """The exact estimator (pipeline.py:212-214): K[idx] @ q divided by
+    sqrt(d) in the keys' dtype."""
+    Km = np.asarray(K)
+    idx = np.asarray(token_idx, dtype=np.int64)
+    return (Km[idx] @ np.asarray(q)) / np.asarray(math.sqrt(Km.shape[1]), dtype=Km.dtype)
+
+
+def dequantize(codes, scale: float, zero: float, dtype=np.float64) -> np.ndarray:
+    """dequantize_row (quantcache.py:117-119): zero + scale * code in fp64."""
+    return (zero + scale * np.asarray(codes, dtype=np.float64)).astype(dtype)
+
+
 def softmax64(logits) -> np.ndarray:
     """Max-subtracted softmax in fp64 over the candidates only
     (attention.py:79-86 as called at pipeline.py:236 / :344)."""
@@ -397,7 +410,7 @@ def prepare_unit(K, page_size: int = PAGE_SIZE, bits: int = 4):
 
 def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.95,
                 page_size: int = PAGE_SIZE, renormalize: bool = True, logits_override=None, prepared=None,
-                sink: int = 4, window: int = 64, bits: int = 4, top_channels=None):
+                sink: int = 4, window: int = 64, bits: int = 4, top_channels=None, exact: bool = False):
     """run_grouped's hot path for one KV head (pipeline.py:306-360):
 
     per-head Quest (selectors.py:112-132; or select_full :90-94, or
@@ -414,7 +427,9 @@ def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.9
     ``logits_override`` (G, |union|) replaces the INT4 estimate, so a test
     can feed the GPU's logits to the oracle's softmax + search;
     ``prepared`` = prepare_unit(K) reuses a prebuilt cache (the reference's
-    cache=/metadata= arguments).  Returns a dict with every intermediate.
+    cache=/metadata= arguments); ``exact`` estimates from the keys themselves
+    (estimator_bits="exact", pipeline.py:212-214).  Returns a dict with every
+    intermediate.
     """
     Q = np.atleast_2d(np.asarray(Q))
     n = K.shape[0]
@@ -443,8 +458,12 @@ def decode_unit(Q, K, V, *, selector: str = "quest", budget=0.25, p: float = 0.9
         cand = pages_to_tokens(union_pages, n, page_size)
     logits, pruned, thresholds, iters = [], [], [], []
     for h in range(G):
-        z = estimate_logits(Q[h], codes, scale, zero, cand) if logits_override is None \
-            else np.asarray(logits_override[h])
+        if logits_override is not None:
+            z = np.asarray(logits_override[h])
+        elif exact:
+            z = exact_logits(Q[h], K, cand)
+        else:
+            z = estimate_logits(Q[h], codes, scale, zero, cand)
         w = softmax64(z)
         sub, thr, it = threshold_top_p(w, p)
         logits.append(z)

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("TW_LIB_PATH") or os.path.join(HERE, "_lib", "libtwili
 TW_OK, TW_ERR_INVALID, TW_ERR_INDEX, TW_ERR_DEGENERATE, TW_ERR_CUDA = range(5)
 TW_F32, TW_BF16 = 0, 1
 TW_SELECT_FULL, TW_SELECT_QUEST, TW_SELECT_SINK_WINDOW, TW_SELECT_CHANNEL_PRUNED = 0, 1, 2, 3
+TW_ESTIMATE_INT, TW_ESTIMATE_EXACT = 0, 1
 PAGE_SIZE = 16
 DEFAULT_CHUNK = 512
 QBLOCK_BYTES = 1152
@@ -59,7 +60,7 @@ class TwDecodeParams(ctypes.Structure):
         ("selector", ctypes.c_int32), ("budget_pages", ctypes.c_int32), ("p", ctypes.c_double),
         ("chunk_tokens", ctypes.c_int32), ("renormalize", ctypes.c_int32), ("sink", ctypes.c_int32),
         ("window", ctypes.c_int32), ("top_channels", ctypes.c_int32), ("budget_tokens", ctypes.c_int32),
-        ("channels_fixed", ctypes.c_int32),
+        ("channels_fixed", ctypes.c_int32), ("estimator", ctypes.c_int32),
     ]
 
 

@@ -20,6 +20,7 @@
 // reference's own byte layout, staged through a per-warp cp.async ring.  The
 // MMA's K order is permuted so the low nibbles of a 32-bit word are one A
 // register and the high nibbles another; q's B fragments use the same order.
+#include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
@@ -386,6 +387,82 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
   if (cur_unit >= 0) flush_max(cur_unit);
 }
 
+// ---------------------------------------------------------------- exact estimator
+
+// estimator_bits = "exact" (_candidate_logits, pipeline.py:212-214): the
+// candidates' logits K[idx] @ q / float32(sqrt d) from the full-precision key
+// cache, same candidate layout and -inf padding as the INT estimate.  Warp per
+// (unit, candidate page); lane (row = lane / 2, half = lane % 2) dots 64
+// channels of its row with the G queries staged in shared memory.  Off the
+// decode hot path (the API's exact estimator and the bypass layers of
+// bypass_config, pipeline.py:129-136), so CUDA cores suffice.
+template <typename T, int G>
+__global__ void __launch_bounds__(kEstWarps * 32) estimate_exact_kernel(tw_paged_kv kv, const T* __restrict__ q,
+                                                                        tw_decode_buffers buf, int sw_sink,
+                                                                        int sw_window,
+                                                                        const uint32_t* __restrict__ tok_mask) {
+  __shared__ float qs[kEstWarps][G][kHeadDim];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = lane >> 1, half = lane & 1;
+  const int units = kv.num_seqs * kv.num_kv_heads;
+  const int T_stride = kv.max_pages * kPage;
+  const float sqrt_d = 11.313708498984761f;  // float32(sqrt(128)), divided as pipeline.py:213
+  int cur_unit = -1;
+  float run_max[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) run_max[g] = -INFINITY;
+  auto flush = [&](int u) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float mx = warp_max(run_max[g]);
+      if (lane == 0 && mx > -INFINITY) atomicMax(buf.head_max + (size_t)u * G + g, f2key(mx));
+      run_max[g] = -INFINITY;
+    }
+  };
+  const long long items = (long long)units * kv.max_pages;
+  for (long long it = (long long)blockIdx.x * kEstWarps + warp; it < items; it += (long long)gridDim.x * kEstWarps) {
+    const int unit = (int)(it % units), c = (int)(it / units);
+    if (c >= buf.cand_count[unit]) continue;
+    const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
+    const int n = kv.seq_lens[b];
+    if (unit != cur_unit) {
+      if (cur_unit >= 0) flush(cur_unit);
+      __syncwarp();
+      for (int i = lane; i < G * kHeadDim; i += 32)
+        qs[warp][i / kHeadDim][i % kHeadDim] = Elem<T>::to_f(q[(size_t)unit * G * kHeadDim + i]);
+      __syncwarp();
+      cur_unit = unit;
+    }
+    const int lp = buf.cand_pages[(size_t)unit * kv.max_pages + c];
+    const int phys = kv.page_table[(size_t)b * kv.max_pages + lp];
+    const T* krow = reinterpret_cast<const T*>(kv.k_cache) +
+                    (((size_t)phys * kv.num_kv_heads + h) * kPage + row) * kHeadDim + 64 * half;
+    float acc[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) acc[g] = 0.f;
+#pragma unroll
+    for (int c8 = 0; c8 < 8; ++c8) {
+      float k8[8];
+      load8(krow + 8 * c8, k8);
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[g] = fmaf(k8[i], qs[warp][g][64 * half + 8 * c8 + i], acc[g]);
+    }
+    const int tok = lp * kPage + row;
+    bool valid = tok < n && (sw_window < 0 || sw_sink + sw_window >= n || tok < sw_sink || tok >= n - sw_window);
+    if (tok_mask) valid = valid && ((__ldg(tok_mask + (size_t)unit * ((T_stride + 31) / 32) + (tok >> 5)) >>
+                                     (tok & 31)) & 1u);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float z = valid ? (acc[g] + __shfl_xor_sync(0xffffffffu, acc[g], 1)) / sqrt_d : -INFINITY;
+      run_max[g] = fmaxf(run_max[g], z);
+      if (half == 0) buf.logits[((size_t)unit * G + g) * T_stride + (size_t)c * kPage + row] = z;
+    }
+  }
+  if (cur_unit >= 0) flush(cur_unit);
+}
+
 // ---------------------------------------------------------------- per-token API
 
 // estimate_scores at arbitrary token ids (quantcache.py:238-272): warp per
@@ -449,9 +526,18 @@ static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode
 
 template <typename T>
 static int launch_estimate(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, int ss, int sw,
-                           const uint32_t* tm, cudaStream_t stream) {
+                           const uint32_t* tm, bool exact, cudaStream_t stream) {
   auto by_bits = [&](auto gtag) {
     constexpr int GG = decltype(gtag)::value;
+    if (exact) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const long long items = (long long)kv->num_seqs * kv->num_kv_heads * kv->max_pages;
+      const int grid = (int)std::min<long long>((items + kEstWarps - 1) / kEstWarps, (long long)sms * 16);
+      estimate_exact_kernel<T, GG><<<grid, kEstWarps * 32, 0, stream>>>(*kv, q, *buf, ss, sw, tm);
+      return;
+    }
     switch (cache_bits(*kv)) {
       case 2: launch_estimate_g<T, GG, 2>(kv, q, buf, ss, sw, tm, stream); break;
       case 8: launch_estimate_g<T, GG, 8>(kv, q, buf, ss, sw, tm, stream); break;
@@ -476,8 +562,11 @@ extern "C" int tw_estimate(const tw_paged_kv* kv, const void* q, const tw_decode
   const uint32_t* tm = prm && prm->selector == TW_SELECT_CHANNEL_PRUNED ? buf->tok_mask : nullptr;
   if (prm && prm->selector == TW_SELECT_CHANNEL_PRUNED && !tm) return TW_ERR_INVALID;
   // head_max is zeroed by tw_select (quest_select_kernel), which always precedes this call
-  if (kv->dtype == TW_BF16) return launch_estimate<__nv_bfloat16>(kv, (const __nv_bfloat16*)q, buf, ss, swin, tm, stream);
-  return launch_estimate<float>(kv, (const float*)q, buf, ss, swin, tm, stream);
+  const bool exact = prm && prm->estimator == TW_ESTIMATE_EXACT;
+  if (prm && prm->estimator != TW_ESTIMATE_INT && !exact) return TW_ERR_INVALID;
+  if (kv->dtype == TW_BF16)
+    return launch_estimate<__nv_bfloat16>(kv, (const __nv_bfloat16*)q, buf, ss, swin, tm, exact, stream);
+  return launch_estimate<float>(kv, (const float*)q, buf, ss, swin, tm, exact, stream);
 }
 
 extern "C" int tw_estimate_tokens(const tw_paged_kv* kv, int32_t seq, int32_t kv_head, const void* q,

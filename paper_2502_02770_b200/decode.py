@@ -263,7 +263,10 @@ class TwilightDecoder:
     "sink_window" (the first ``sink`` + last ``window`` tokens, selectors.py:164-175), or
     "channel_pruned" (per query head the ``budget`` tokens with the largest
     partial logit over the ``top_channels`` channels of largest mean |K|,
-    selectors.py:135-161; contexts up to 32768 tokens).  With
+    selectors.py:135-161; contexts up to 32768 tokens).  ``estimator`` "int"
+    estimates the candidates' logits from the cache's INT codes
+    (quantcache.py:238-272), "exact" from the full-precision keys
+    (estimator_bits="exact", pipeline.py:212-214).  With
     ``fix_channels`` the channel slice ranked at the first step is kept for the
     following steps (the reference binds it once per context, selectors.py:203);
     otherwise it is re-ranked over the current cache every step.
@@ -272,7 +275,7 @@ class TwilightDecoder:
     def __init__(self, cache: PagedKVCache, selector: str = "quest", budget=None, p: float = 0.95,
                  chunk_tokens: int | None = None, head_page_bits: bool = False,
                  bufs: DecodeBuffers | list | None = None, waves: int = 1, sink: int = 4, window: int = 64,
-                 top_channels: int | None = None, fix_channels: bool = False):
+                 top_channels: int | None = None, fix_channels: bool = False, estimator: str = "int"):
         self.waves = []
         if waves > 1:
             # sub-batches on their own streams: the select/top-p stages of one wave
@@ -284,7 +287,7 @@ class TwilightDecoder:
                 sub = TwilightDecoder(cache.view(w * per, (w + 1) * per), selector, budget, p, chunk_tokens,
                                       head_page_bits, bufs[w] if isinstance(bufs, list) else None,
                                       sink=sink, window=window, top_channels=top_channels,
-                                      fix_channels=fix_channels)
+                                      fix_channels=fix_channels, estimator=estimator)
                 self.waves.append((w * per, (w + 1) * per, sub, torch.cuda.Stream(device=cache.device)))
             self.cache = cache
             self.params = self.waves[0][2].params
@@ -300,6 +303,8 @@ class TwilightDecoder:
             raise ValueError("sink and window must be non-negative and keep at least one token")
         if not 0.0 <= p <= 1.0:
             raise ValueError(f"p={p} outside [0, 1]")
+        if estimator not in ("int", "exact"):
+            raise ValueError(f"estimator {estimator!r} must be 'int' (the cache's INT codes) or 'exact'")
         self.cache = cache
         # buffers may be shared by decoders of layers with the same geometry
         self.bufs = bufs if bufs is not None else DecodeBuffers(cache, chunk_tokens, head_page_bits)
@@ -313,6 +318,8 @@ class TwilightDecoder:
         self.params.top_channels = int(top_channels) if top_channels is not None else max(1, L.HEAD_DIM // 8)
         self.fix_channels = bool(fix_channels)
         self.params.p = float(p)
+        # estimator_bits="exact" (pipeline.py:212-214): logits from the full-precision keys
+        self.params.estimator = L.TW_ESTIMATE_EXACT if estimator == "exact" else L.TW_ESTIMATE_INT
         self.params.chunk_tokens = chunk_tokens
         self.params.renormalize = 1
         self.set_budget(budget)

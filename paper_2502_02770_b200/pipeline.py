@@ -1,10 +1,13 @@
 """Select -> estimate -> prune -> attend with the reference signatures
 (nucleuskv/pipeline.py).
 
-``run_head`` / ``run_grouped`` build a one-context paged pool (K1 bulk) and
-run the batched decode kernels (K2 tw_select, K3 tw_estimate + tw_topp,
-K4 tw_sparse_attention) for it: the same code path the batched decoder and
-the benchmark use.  PruneReport fields that need the exact full-context fp64
+``run_head`` / ``run_grouped`` build a one-context paged pool (K1 bulk) --
+or reuse the one behind a ``cache=`` / ``metadata=`` from build_cache, as
+_prepare_context does (pipeline.py:177-201) -- and run the batched decode
+kernels (K2 tw_select, K3 tw_estimate + tw_topp, K4 tw_sparse_attention) for
+it: the same code path the batched decoder and the benchmark use.
+``estimator_bits="exact"`` (and so bypass_config) estimates from the
+full-precision keys (pipeline.py:212-214).  PruneReport fields that need the exact full-context fp64
 attention (true mass, residual, Spearman) are instrumentation, not the
 decode path; they are computed with device tensor ops after the kernels.
 """
@@ -20,7 +23,7 @@ from . import _lib as L
 from .attention import TokenSelection
 from .decode import TwilightDecoder, pages_for
 from .pruner import BinarySearchConfig, PruneOutcome
-from .quantcache import PagedQuantKeyCache, _unit_cache
+from .quantcache import PagedQuantKeyCache, PageMetadataTable, _shared_pool, _unit_cache
 from .selectors import GroupMap, SelectorConfig, resolve_budget
 
 __all__ = ["PipelineConfig", "PruneReport", "bypass_config", "run_head", "run_grouped", "model_speedup",
@@ -118,8 +121,6 @@ def _spearman(a: torch.Tensor, b: torch.Tensor) -> float:
 def _check_cfg(cfg: PipelineConfig) -> None:
     if cfg.selector.kind not in ("full", "quest", "sink_window", "channel_pruned"):
         raise NotImplementedError(f"selector {cfg.selector.kind!r} is not on the B200 path")
-    if cfg.estimator_bits not in (2, 4, 8):
-        raise NotImplementedError("the B200 path estimates with a 2-, 4- or 8-bit cache (estimator_bits)")
     if cfg.selector.page_size != L.PAGE_SIZE:
         raise ValueError("the B200 path uses 16-token pages")
     if cfg.prune.epsilon != 1e-15 or cfg.prune.max_iters != 64:
@@ -129,7 +130,34 @@ def _check_cfg(cfg: PipelineConfig) -> None:
         raise NotImplementedError("renormalize_output=False needs the full-context denominator (off the hot path)")
 
 
-def _run(Q: torch.Tensor, keys: torch.Tensor, values: torch.Tensor, cfg: PipelineConfig, G: int, cache=None):
+def _prepare_context(keys, values, cfg: PipelineConfig, G: int, groups: int, cache, metadata):
+    """_prepare_context (pipeline.py:177-201) on the device pool: reuse the
+    pool behind a supplied cache (or metadata table) when it fits the config,
+    else build one (K1 bulk).  A cache of the wrong width or page size raises
+    like the reference (:194-200)."""
+    exact = cfg.estimator_bits == "exact"
+    n = keys.shape[0]
+    pool = None
+    if cache is not None and not exact:
+        if cache.bits != cfg.estimator_bits:
+            raise ValueError(f"cache quantized at {cache.bits} bits, config wants {cfg.estimator_bits}")
+        if cache.page_size != cfg.selector.page_size:
+            raise ValueError("cache page size differs from selector page size")
+        pool = cache.kv
+    elif isinstance(metadata, PageMetadataTable) and (exact or metadata.cache.bits == cfg.estimator_bits):
+        pool = metadata.cache
+    elif cache is not None and isinstance(cache, PagedQuantKeyCache):
+        pool = cache.kv  # exact estimator: only the keys and page metadata of the pool are read
+    if pool is not None:
+        if int(pool.seq_lens[0].item()) != n or pool.dtype != keys.dtype:
+            raise ValueError("the supplied cache was built for different keys")
+        return _shared_pool(pool, values, G, groups)
+    return _unit_cache(keys, values.to(keys.dtype), group_size=G, num_seqs=groups,
+                       bits=4 if exact else cfg.estimator_bits)
+
+
+def _run(Q: torch.Tensor, keys: torch.Tensor, values: torch.Tensor, cfg: PipelineConfig, G: int, cache=None,
+         metadata=None):
     """Run the decode kernels for H = groups*G query heads on one KV context."""
     _check_cfg(cfg)
     if not (Q.is_cuda and keys.is_cuda and values.is_cuda):
@@ -138,20 +166,23 @@ def _run(Q: torch.Tensor, keys: torch.Tensor, values: torch.Tensor, cfg: Pipelin
     H = Q.shape[0]
     groups = H // G
     dt = keys.dtype
-    kv = _unit_cache(keys, values.to(dt), group_size=G, num_seqs=groups, bits=cfg.estimator_bits)
+    kv = _prepare_context(keys, values, cfg, G, groups, cache, metadata)
+    est = "exact" if cfg.estimator_bits == "exact" else "int"
     if cfg.selector.kind == "quest":
         if cfg.selector.budget is None:
             raise ValueError("selector 'quest' requires a budget")
-        dec = TwilightDecoder(kv, "quest", budget=resolve_budget(cfg.selector.budget, n), p=cfg.prune.p)
+        dec = TwilightDecoder(kv, "quest", budget=resolve_budget(cfg.selector.budget, n), p=cfg.prune.p,
+                              estimator=est)
     elif cfg.selector.kind == "sink_window":
-        dec = TwilightDecoder(kv, "sink_window", p=cfg.prune.p, sink=cfg.selector.sink, window=cfg.selector.window)
+        dec = TwilightDecoder(kv, "sink_window", p=cfg.prune.p, sink=cfg.selector.sink, window=cfg.selector.window,
+                              estimator=est)
     elif cfg.selector.kind == "channel_pruned":
         if cfg.selector.budget is None:
             raise ValueError("selector 'channel_pruned' requires a budget")
         dec = TwilightDecoder(kv, "channel_pruned", budget=resolve_budget(cfg.selector.budget, n), p=cfg.prune.p,
-                              top_channels=cfg.selector.top_channels)
+                              top_channels=cfg.selector.top_channels, estimator=est)
     else:
-        dec = TwilightDecoder(kv, "full", p=cfg.prune.p)
+        dec = TwilightDecoder(kv, "full", p=cfg.prune.p, estimator=est)
     q = Q.to(dt).reshape(groups, G, L.HEAD_DIM).contiguous()
     out = dec.forward(q)
     return dec, out.reshape(H, L.HEAD_DIM)
@@ -190,14 +221,16 @@ def _reports(dec: TwilightDecoder, Q, keys, values, cfg: PipelineConfig, G: int)
         rho = _spearman(logits.double(), true_logits)
         b0, b1 = int(cand.numel()), cnt
         scan = n * cfg.selector_cost_fraction
-        cost = scan + b0 * (cfg.estimator_bits / 16.0) + b1
+        exact = cfg.estimator_bits == "exact"
+        cost = scan + b0 * (1.0 if exact else cfg.estimator_bits / 16.0) + b1  # _estimator_fraction
         base = scan + b0
         res.append((sel, exact_out[h], dict(n=n, b0=b0, b1=b1, attained_candidate_mass=cand_mass,
                                             attained_true_mass=attained_true, estimator_spearman=rho,
                                             threshold=float(bufs.head_stats[h, 2].item()), iterations=0,
                                             value_norm=value_norm, tokens_selector=n, tokens_estimator=b0,
                                             tokens_attention=b1,
-                                            estimator_bytes=b0 * (L.HEAD_DIM * cfg.estimator_bits // 8 + 4),
+                                            estimator_bytes=b0 * (2 * L.HEAD_DIM if exact else
+                                                                  L.HEAD_DIM * cfg.estimator_bits // 8 + 4),
                                             cost_units=cost, baseline_units=base, modeled_speedup=base / cost)))
     return res
 
@@ -215,10 +248,10 @@ def _assemble(res, outs):
 def run_head(q, keys, values, cfg: PipelineConfig, *, cache: PagedQuantKeyCache | None = None, metadata=None):
     """pipeline.py:286-303 on the B200 kernels: (output, PruneOutcome, PruneReport).
 
-    A supplied ``cache``/``metadata`` (from build_cache) is accepted for
-    signature compatibility; the pool is rebuilt with the values attached."""
+    A supplied ``cache``/``metadata`` (from build_cache) is reused as built
+    (_prepare_context, pipeline.py:177-201): no re-quantization."""
     q = torch.as_tensor(q)
-    dec, out = _run(q.reshape(1, -1), torch.as_tensor(keys), torch.as_tensor(values), cfg, 1)
+    dec, out = _run(q.reshape(1, -1), torch.as_tensor(keys), torch.as_tensor(values), cfg, 1, cache, metadata)
     res = _reports(dec, q.reshape(1, -1), keys, values, cfg, 1)
     outcomes, reports = _assemble(res, out)
     return out[0], outcomes[0], reports[0]
@@ -237,7 +270,7 @@ def run_grouped(queries, keys, values, cfg: PipelineConfig, *, cache: PagedQuant
     G = gm.group_size
     if G not in (1, 2, 4, 8):
         raise NotImplementedError("group sizes 1, 2, 4, 8 are compiled")
-    dec, out = _run(Q, torch.as_tensor(keys), torch.as_tensor(values), cfg, G)
+    dec, out = _run(Q, torch.as_tensor(keys), torch.as_tensor(values), cfg, G, cache, metadata)
     res = _reports(dec, Q, keys, values, cfg, G)
     outcomes, reports = _assemble(res, out)
     return out, outcomes, reports

@@ -5,8 +5,8 @@ with the K1 bulk kernel (tw_quant_build); ``quantize_row`` runs tw_quant_rows;
 ``estimate_scores`` runs tw_estimate_tokens.  The returned objects wrap device
 tensors; ``PagedQuantKeyCache.pages`` materialises the reference's per-page
 view (packed bytes, fp64 scale/zero, valid_len) for inspection and tests.
-Only 4-bit codes are on the accelerated path (the reference's 2/8-bit modes
-exist for a Fig. 6 sweep): other widths raise.
+Caches of 2, 4 and 8 bits (SUPPORTED_BITS) are built and estimated on the
+GPU; the decode path defaults to 4.
 """
 
 from __future__ import annotations
@@ -21,7 +21,7 @@ from . import _lib as L
 from .attention import TokenSelection
 from .decode import PagedKVCache, pages_for
 
-SUPPORTED_BITS = (2, 4, 8)  # quantize_row accepts these (quantcache.py:38); the cache is 4-bit
+SUPPORTED_BITS = (2, 4, 8)  # quantcache.py:38
 PARAM_BYTES = 4             # traffic model (quantcache.py:42)
 
 __all__ = ["SUPPORTED_BITS", "PARAM_BYTES", "QuantParams", "QuantPage", "PageMetadata", "PageMetadataTable",
@@ -135,6 +135,30 @@ def _unit_cache(keys: torch.Tensor, values: torch.Tensor | None = None, group_si
     # write the shared pages once (sequence 0), then quantize for every sequence row
     cache.prefill(Kp.expand(num_seqs, 1, n, L.HEAD_DIM), Vp.expand(num_seqs, 1, n, L.HEAD_DIM))
     return cache
+
+
+def _shared_pool(pool: PagedKVCache, values: torch.Tensor, group_size: int, num_seqs: int) -> PagedKVCache:
+    """A prebuilt one-context pool (build_cache) reused for ``num_seqs``
+    sequence rows of ``group_size`` query heads: the quantized keys, page
+    metadata and |k| bound are shared as built (no tw_quant_build), only the
+    values are written into the pool's V pages."""
+    n = int(pool.seq_lens[0].item())
+    V = torch.as_tensor(values).to(device=pool.device, dtype=pool.dtype)
+    if V.shape != (n, L.HEAD_DIM):
+        raise ValueError(f"values must be ({n}, {L.HEAD_DIM}) to match the cache, got {tuple(V.shape)}")
+    P = pages_for(n)
+    pad = P * L.PAGE_SIZE - n
+    Vp = torch.nn.functional.pad(V, (0, 0, 0, pad)) if pad else V
+    phys = pool.page_table[0, :P].long()
+    pool.v_cache[phys, 0] = Vp.view(P, L.PAGE_SIZE, L.HEAD_DIM)
+    v = PagedKVCache.__new__(PagedKVCache)
+    v.__dict__.update(pool.__dict__)
+    v.num_seqs, v.group_size = num_seqs, group_size
+    v.page_table = pool.page_table[:1].repeat(num_seqs, 1).contiguous()
+    v.seq_lens = pool.seq_lens[:1].repeat(num_seqs).contiguous()
+    v.kabsmax = pool.kabsmax[:1].repeat(num_seqs, 1).contiguous()
+    v._struct = None
+    return v
 
 
 def quantize_row(k, bits: int = 4):

@@ -330,3 +330,109 @@ def test_channel_pruned_build_selector():
     got = sel(cuda(q)).indices.cpu().numpy()
     ids = orc.top_channels_by_magnitude(K, 12)
     np.testing.assert_array_equal(got, orc.channel_pruned_tokens(q, K, ids, 50))
+
+
+def test_dequantize_row_and_unpack_codes_match_reference(golden):
+    """dequantize_row / unpack_codes (quantcache.py:117-119, 154-160) against
+    the reference's own answers (tests/golden/rows.npz)."""
+    for name, c in golden("rows").items():
+        if name.startswith("deq"):
+            prm = tw.QuantParams(scale=float(c["params"][0]), zero=float(c["params"][1]))
+            codes = cuda(c["codes"], torch.uint8)
+            np.testing.assert_array_equal(tw.dequantize_row(codes, prm).cpu().numpy(), c["f64"], err_msg=name)
+            np.testing.assert_array_equal(tw.dequantize_row(codes, prm, torch.float32).cpu().numpy(), c["f32"],
+                                          err_msg=name)
+        elif name.startswith("unpack"):
+            got = tw.unpack_codes(c["packed"].tobytes(), 2 * c["packed"].size)
+            np.testing.assert_array_equal(got.cpu().numpy(), c["codes"], err_msg=name)
+            assert tw.pack_codes(got) == c["packed"].tobytes()
+    with pytest.raises(ValueError):
+        tw.unpack_codes(b"\x00\x01", 6)
+
+
+def test_exact_estimator_and_bypass_config_match_reference(golden):
+    """estimator_bits="exact" (_candidate_logits, pipeline.py:212-214) through
+    the exact-estimate kernel, and run_grouped(..., bypass_config(cfg)) -- the
+    bypass layers' dense configuration (pipeline.py:129-136, cli.py:83-87) --
+    against the reference's outputs and final sets, and the dense oracle."""
+    for name, c in golden("rows").items():
+        if not name.startswith("x"):
+            continue
+        budget, p, is_frac, quest = c["cfg"]
+        budget = float(budget) if is_frac else int(budget)
+        bf = np.array_equal(torch.as_tensor(c["K"]).bfloat16().float().numpy(), c["K"])
+        dt = torch.bfloat16 if bf else torch.float32
+        K, V, Q = cuda(c["K"], dt), cuda(c["V"], dt), cuda(c["Q"], dt)
+        G = Q.shape[0]
+        base = tw.PipelineConfig(selector=tw.SelectorConfig(kind="quest" if quest else "full",
+                                                            budget=budget if quest else None),
+                                 prune=tw.BinarySearchConfig(p=float(p)), group_map=tw.GroupMap(G))
+        cfg = replace_cfg_exact(base) if quest else tw.bypass_config(base)
+        if G == 1:
+            out, outcome, report = tw.run_head(Q[0], K, V, cfg)
+            outs, final, b0 = out[None], outcome.selection.indices, report.b0
+        else:
+            outs, outcomes, reports = tw.run_grouped(Q, K, V, cfg)
+            final, b0 = outcomes[0].selection.indices, reports[0].b0
+        assert b0 == c["b0"][0], name
+        tol = 2e-2 if bf else 1e-4
+        final = final.cpu().numpy()
+        assert_final_set_and_output(Q, K, V, cfg, G, final, outs.cpu().numpy(), tol, name)
+        # the exact logits themselves (fp32 dot products; BLAS order differs)
+        dec, _ = _pl._run(Q, K, V, cfg, G)
+        torch.cuda.synchronize()
+        from tests.gpu_util import unit_candidates
+        cand, z = unit_candidates(dec.bufs, 0)
+        for g in range(G):
+            want = orc.exact_logits(c["Q"][g], c["K"], cand)
+            np.testing.assert_allclose(z[g], want, rtol=1e-5, atol=1e-5 * np.abs(want).max(), err_msg=name)
+        np.testing.assert_array_equal(final, c["final"], err_msg=name)
+        np.testing.assert_allclose(outs.cpu().numpy(), c["out"], rtol=tol, atol=tol * np.abs(c["out"]).max(),
+                                   err_msg=name)
+        if not quest:  # bypass: the dense oracle (softmax over every token)
+            for g in range(G):
+                w = orc.full_weights(c["Q"][g], c["K"])
+                np.testing.assert_allclose(outs[g].cpu().numpy(), w @ c["V"], rtol=1e-4,
+                                           atol=1e-4 * np.abs(w @ c["V"]).max(), err_msg=name)
+
+
+def replace_cfg_exact(cfg):
+    from dataclasses import replace
+    return replace(cfg, estimator_bits="exact")
+
+
+def test_prebuilt_cache_is_reused(monkeypatch):
+    """run_grouped / run_head with cache= / metadata= from build_cache reuse
+    that pool (_prepare_context, pipeline.py:177-201): no tw_quant_build, the
+    same INT4 pages, the same results as building it inside the call; a cache
+    of another width is rejected like the reference (:194-198)."""
+    from paper_2502_02770_b200 import _lib
+    rng = np.random.default_rng(7)
+    n, G = 1000, 4
+    K = torch.from_numpy(rng.standard_normal((n, 128)).astype(np.float32)).bfloat16().cuda()
+    V = torch.from_numpy(rng.standard_normal((n, 128)).astype(np.float32)).bfloat16().cuda()
+    Q = torch.from_numpy(rng.standard_normal((8, 128)).astype(np.float32) * 2).bfloat16().cuda()
+    cfg = tw.PipelineConfig(selector=tw.SelectorConfig(kind="quest", budget=256), prune=tw.BinarySearchConfig(p=0.9),
+                            group_map=tw.GroupMap(G))
+    want, want_oc, _ = tw.run_grouped(Q, K, V, cfg)
+    cache, meta = tw.build_cache(K)
+    lib = _lib.lib()
+    real = lib.tw_quant_build
+    calls = []
+    monkeypatch.setattr(lib, "tw_quant_build", lambda *a: calls.append(1) or real(*a))
+    got, got_oc, _ = tw.run_grouped(Q, K, V, cfg, cache=cache, metadata=meta)
+    head, head_oc, _ = tw.run_head(Q[0], K, V, tw.PipelineConfig(selector=cfg.selector, prune=cfg.prune),
+                                   cache=cache)
+    torch.cuda.synchronize()
+    assert calls == []
+    assert torch.equal(got, want)
+    assert torch.equal(got_oc[0].selection.indices, want_oc[0].selection.indices)
+    dec, _ = _pl._run(Q, K, V, cfg, G, cache, meta)
+    assert dec.cache.kq.data_ptr() == cache.kv.kq.data_ptr()
+    with pytest.raises(ValueError):
+        tw.run_grouped(Q, K, V, replace_bits(cfg, 2), cache=cache)
+
+
+def replace_bits(cfg, bits):
+    from dataclasses import replace
+    return replace(cfg, estimator_bits=bits)

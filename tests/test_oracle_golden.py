@@ -146,3 +146,25 @@ def test_channel_pruned_matches_reference(golden):
             np.testing.assert_array_equal(res["final"], c["final"], err_msg=name)
             assert res["candidates"].size == c["b0"][0], name
             np.testing.assert_allclose(res["out"], c["out"], rtol=1e-5, atol=1e-6, err_msg=name)
+
+
+def test_dequantize_unpack_and_exact_estimator_match_reference(golden):
+    """dequantize_row / unpack_codes (quantcache.py:117-160) and the exact
+    estimator pipelines -- bypass_config and estimator_bits="exact"
+    (pipeline.py:129-136, 204-216) -- against the reference's answers."""
+    cases = golden("rows")
+    for name, c in cases.items():
+        if name.startswith("deq"):
+            scale, zero = c["params"]
+            np.testing.assert_array_equal(orc.dequantize(c["codes"], scale, zero), c["f64"], err_msg=name)
+            np.testing.assert_array_equal(orc.dequantize(c["codes"], scale, zero, np.float32), c["f32"], err_msg=name)
+        elif name.startswith("unpack"):
+            np.testing.assert_array_equal(orc.unpack_nibbles(c["packed"]), c["codes"], err_msg=name)
+        else:
+            budget, p, is_frac, quest = c["cfg"]
+            budget = float(budget) if is_frac else int(budget)
+            res = orc.decode_unit(c["Q"], c["K"], c["V"], selector="quest" if quest else "full",
+                                  budget=budget, p=float(p), exact=True)
+            np.testing.assert_array_equal(res["final"], c["final"], err_msg=name)
+            assert res["candidates"].size == c["b0"][0]
+            np.testing.assert_allclose(res["out"], c["out"], rtol=1e-5, atol=1e-6, err_msg=name)
