@@ -186,19 +186,31 @@ def algorithmic_bytes(cfg, dec, n, elem=2):
     k4 = F * (2 * d * elem + 4) + units * G * d * (elem + 4)                  # gathered K,V rows + q + out
     dense = units * n * 2 * d * elem + units * G * d * (elem + 4)
     return {"K1_append": k1, "K2_select": k2, "K3a_estimate": k3a, "K3bc_topp": k3bc, "K4_attention": k4,
-            "step": k1 + k2 + k3a + k3bc + k4, "K5_dense": dense, "cand_pages": U, "final_tokens": F}
+            "K23_unit": k2 + k3a + k3bc, "step": k1 + k2 + k3a + k3bc + k4, "K5_dense": dense, "cand_pages": U, "final_tokens": F}
 
 
 STAGE_NAMES = ["K1_append", "K2_select", "K3a_estimate", "K3bc_topp", "K4_attention"]
+# the fused per-unit kernel (tw_select_estimate_topp) runs K2 + K3 as one launch
+UNIT_STAGE_NAMES = ["K1_append", "K23_unit", "K4_attention"]
+
+
+def stage_names(dec):
+    return UNIT_STAGE_NAMES if dec.unit_path else STAGE_NAMES
 
 
 def stage_breakdown(decs, q, k_new, v_new, positions, out, reps):
     """Mean µs of each stage (K1..K4) per step: every stage captured in its own
-    CUDA graph, CUDA events between replays, rotating over `decs`."""
+    CUDA graph, CUDA events between replays, rotating over `decs`.  With the
+    fused per-unit kernel the stages are K1, K2+K3 (one launch), K4."""
     stream = torch.cuda.current_stream()
     B = q.shape[0]
+    names = stage_names(decs[0])
 
     def stage_fns(dec):
+        if dec.unit_path:
+            return [lambda: dec.cache.append(k_new, v_new, positions),
+                    lambda: dec.select_estimate_topp(q),
+                    lambda: dec.attend(q, out)]
         subs = [(lo, hi, s) for lo, hi, s, _ in dec.waves] if dec.waves else [(0, B, dec)]
         return [lambda: dec.cache.append(k_new, v_new, positions),
                 lambda: [s.select(q[lo:hi]) for lo, hi, s in subs],
@@ -214,8 +226,8 @@ def stage_breakdown(decs, q, k_new, v_new, positions, out, reps):
                 fn()
             row.append(g)
         stage_graphs.append(row)
-    stage_ms = {k: 0.0 for k in STAGE_NAMES}
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(STAGE_NAMES) + 1)]
+    stage_ms = {k: 0.0 for k in names}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
     for i in range(reps + 1):
         ev[0].record(stream)
         for j, g in enumerate(stage_graphs[i % len(decs)]):
@@ -224,7 +236,7 @@ def stage_breakdown(decs, q, k_new, v_new, positions, out, reps):
         torch.cuda.synchronize()
         if i == 0:
             continue
-        for j, k in enumerate(STAGE_NAMES):
+        for j, k in enumerate(names):
             stage_ms[k] += ev[j].elapsed_time(ev[j + 1]) / reps
     return stage_ms
 
@@ -390,8 +402,8 @@ def run_ours(args, cfg):
     dec0 = decs[(args.steps - 1) % L]
     ab = algorithmic_bytes(cfg, dec0, n)
     peak, peak_src = load_peak()
-    kernel_gbs = {k: (ab[k] / (stage_ms[k] * 1e-3) / 1e9 if stage_ms[k] > 0 and ab[k] else None) for k in STAGE_NAMES}
-    dominant = max(STAGE_NAMES, key=lambda k: stage_ms[k])
+    kernel_gbs = {k: (ab[k] / (stage_ms[k] * 1e-3) / 1e9 if stage_ms[k] > 0 and ab[k] else None) for k in stage_ms}
+    dominant = max(stage_ms, key=lambda k: stage_ms[k])
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -432,7 +444,7 @@ def run_ours(args, cfg):
                                                     if copies_in_graph else " (step captured)")},
         # quest: filter (+ fused K1 append), select, estimate, top-p, attention, merge;
         # other selectors: append, select, estimate, top-p, attention, merge
-        "gpu_launches": 6 * args.steps,
+        "gpu_launches": (3 if decs[0].unit_path else 6) * args.steps,
         "roofline": {"bound": "hbm", "kernel": dominant,
                      "achieved": round(kernel_gbs[dominant], 1) if kernel_gbs[dominant] else None,
                      "peak": peak, "unit": "GB/s",
@@ -450,7 +462,7 @@ def run_ours(args, cfg):
                           "frac": round(achieved_step / peak, 4)},
         "kernels_us": {k: round(v * 1e3, 2) for k, v in stage_ms.items()},
         "kernels_gbs": {k: (round(v, 1) if v else None) for k, v in kernel_gbs.items()},
-        "algorithmic_bytes": {k: ab[k] for k in STAGE_NAMES},
+        "algorithmic_bytes": {k: ab[k] for k in stage_ms},
         "dense_us_per_layer": round(dense_ms * 1e3, 2),
         "dense_gbs": round(ab["K5_dense"] / (dense_ms * 1e-3) / 1e9, 1),
         "speedup_vs_dense": round(dense_ms / ms, 3),
@@ -570,8 +582,8 @@ def run_model(args, cfg):
     n_dense = L - n_tw
     attn_ms = sum(stage_ms.values()) * n_tw + dense_ms * n_dense
     peak, peak_src = load_peak()
-    kernel_gbs = {k: (ab[k] / (stage_ms[k] * 1e-3) / 1e9 if stage_ms[k] > 0 and ab[k] else None) for k in STAGE_NAMES}
-    dominant = max(STAGE_NAMES, key=lambda k: stage_ms[k])
+    kernel_gbs = {k: (ab[k] / (stage_ms[k] * 1e-3) / 1e9 if stage_ms[k] > 0 and ab[k] else None) for k in stage_ms}
+    dominant = max(stage_ms, key=lambda k: stage_ms[k])
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -606,7 +618,8 @@ def run_model(args, cfg):
         "e2e": {"value": round(e2e_ms * 1e3 / L, 2), "unit": "us/layer", "h2d_bytes_per_step": B * 8,
                 "d2h_bytes_per_step": B * 8,
                 "path": "LlamaTwilightDecoder.step (captured) with token ids from pinned host, argmax ids to host"},
-        "gpu_launches": ((7 if cfg["selector"] == "quest" else 8) * n_tw + 3 * n_dense) * args.steps,
+        "gpu_launches": ((3 if dec.unit_path else 7 if cfg["selector"] == "quest" else 8) * n_tw
+                         + 3 * n_dense) * args.steps,
         "roofline": {"bound": "hbm", "kernel": dominant,
                      "achieved": round(kernel_gbs[dominant], 1) if kernel_gbs[dominant] else None,
                      "peak": peak, "unit": "GB/s",

@@ -190,6 +190,23 @@ int tw_sparse_attention(const tw_paged_kv* kv, const void* q, const tw_decode_pa
 int tw_dense_attention(const tw_paged_kv* kv, const void* q, const tw_decode_buffers* buf,
                        float* out, cudaStream_t stream);
 
+/* K2 + K3 (tw_select, tw_estimate, tw_topp) for every unit in ONE launch, one
+ * CTA per unit (sequence, KV head) running its filter, page selection, INT4
+ * estimate and top-p back to back; with positions (and k_new, v_new) the K1
+ * append of each unit's new row runs first inside the same CTA (positions must
+ * not alias seq_lens).  Same outputs as the separate calls.  Covers bf16
+ * caches with 4-bit codes, the quest and full selectors, the INT estimator,
+ * G in {1, 2, 4} and batches of at least 64 units (TW_UNIT_MIN); anything else
+ * returns TW_ERR_INVALID (use the separate calls).  tw_decode_step takes this
+ * path whenever it applies. */
+int tw_select_estimate_topp(const tw_paged_kv* kv, const void* q, const void* k_new, const void* v_new,
+                            const int32_t* positions, const tw_decode_params* prm,
+                            const tw_decode_buffers* buf, cudaStream_t stream);
+
+/* 1 when tw_select_estimate_topp covers this geometry and these options, else 0. */
+int32_t tw_select_estimate_topp_applies(const tw_paged_kv* kv, const tw_decode_params* prm,
+                                        const tw_decode_buffers* buf);
+
 /* One full decode step of one layer: K1 append, K2, K3a, K3b/c, K4. */
 int tw_decode_step(const tw_paged_kv* kv, const void* q, const void* k_new, const void* v_new,
                    const int32_t* positions, const tw_decode_params* prm,

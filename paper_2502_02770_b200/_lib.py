@@ -35,7 +35,8 @@ TOPP_MEMBER_CAP = 8192    # TW_TOPP_MEMBER_CAP
 EXPORTS = (
     "tw_version", "tw_max_work_items", "tw_quant_append", "tw_quant_build", "tw_quant_rows",
     "tw_quest_scores", "tw_select", "tw_estimate", "tw_topp", "tw_sparse_attention",
-    "tw_dense_attention", "tw_decode_step", "tw_estimate_tokens", "tw_topp_bisect",
+    "tw_dense_attention", "tw_decode_step", "tw_estimate_tokens", "tw_topp_bisect", "tw_select_estimate_topp",
+    "tw_select_estimate_topp_applies",
 )
 
 
@@ -106,6 +107,8 @@ def lib() -> ctypes.CDLL:
         "tw_decode_step": ([P, P, P, P, P, P, P, P, P], ctypes.c_int),
         "tw_estimate_tokens": ([P, I32, I32, P, P, I32, P, P, P], ctypes.c_int),
         "tw_topp_bisect": ([P, I32, I32, ctypes.c_double, ctypes.c_double, I32, P, P, P, P], ctypes.c_int),
+        "tw_select_estimate_topp": ([P, P, P, P, P, P, P, P], ctypes.c_int),
+        "tw_select_estimate_topp_applies": ([P, P, P], I32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

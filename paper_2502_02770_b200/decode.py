@@ -354,6 +354,21 @@ class TwilightDecoder:
         if self.fix_channels and self.params.selector == L.TW_SELECT_CHANNEL_PRUNED:
             self.params.channels_fixed = 1
 
+    @property
+    def unit_path(self) -> bool:
+        """True when K2 + K3 run as the fused per-unit kernel (tw_select_estimate_topp)."""
+        if self.waves:
+            return False
+        kv, prm, buf = self._args()
+        return bool(L.lib().tw_select_estimate_topp_applies(kv, prm, buf))
+
+    def select_estimate_topp(self, q: torch.Tensor, k_new: torch.Tensor | None = None,
+                             v_new: torch.Tensor | None = None, positions: torch.Tensor | None = None) -> None:
+        """K2 + K3 in one per-unit launch; with positions, K1 (the append of k_new/v_new) too."""
+        kv, prm, buf = self._args()
+        L.check(L.lib().tw_select_estimate_topp(kv, L.ptr(q), L.ptr(k_new), L.ptr(v_new), L.ptr(positions), prm,
+                                                buf, L.stream_handle()), "tw_select_estimate_topp")
+
     def estimate(self, q: torch.Tensor) -> None:
         kv, prm, buf = self._args()
         L.check(L.lib().tw_estimate(kv, L.ptr(q), prm, buf, L.stream_handle()), "tw_estimate")
@@ -400,9 +415,12 @@ class TwilightDecoder:
             for lo, hi, sub, _ in self.waves:
                 sub.forward(q[lo:hi], out[lo:hi])
             return out
-        self.select(q)
-        self.estimate(q)
-        self.topp()
+        if self.unit_path:
+            self.select_estimate_topp(q)
+        else:
+            self.select(q)
+            self.estimate(q)
+            self.topp()
         return self.attend(q, out)
 
     def _step_waves(self, q, k_new, v_new, positions, out):
