@@ -49,7 +49,7 @@ CONFIGS = {
                shard="batch", model=True),
     "C5": dict(desc="Llama-3.1-8B shape, batch 32, ctx 128k, Quest n/4 + top-p (p sweep point 0.9), "
                     "focused vs diffuse heads", B=32, H=8, G=4, n=131072, selector="quest", budget=32768, p=0.9,
-               layers=2, shard="batch"),
+               layers=2, shard="batch", p_sweep=(0.8, 0.85, 0.9, 0.95, 0.99)),
 }
 TAUS = (0.25, 0.5, 1.0, 2.0)  # per-KV-head temperatures, cycled: focused .. diffuse
 METRIC = "sparse decode-attn us/layer & achieved HBM GB/s at 32k-128k ctx, 1/2/4/8 GPU"
@@ -160,6 +160,15 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def min_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return float(t.item())
+
+
 def sum_over_ranks(x: float, world: int) -> float:
     if world == 1:
         return x
@@ -241,6 +250,59 @@ def stage_breakdown(decs, q, k_new, v_new, positions, out, reps):
     return stage_ms
 
 
+def head_taus(cfg, H_local, rank, world):
+    """tau of every query head of this rank's decoders, in head_stats order (unit-major)."""
+    H = cfg["H"]
+    taus = [TAUS[h % len(TAUS)] for h in range(H)]
+    if cfg["shard"] == "head":
+        taus = taus[rank * H_local:(rank + 1) * H_local]
+    per_unit = taus[:H_local]
+    return [t for _ in range(cfg["B"]) for t in per_unit for _ in range(cfg["G"])]
+
+
+def sweep_point(args, cfg, decs, q, k_new, v_new, positions, out, p, world):
+    """One point of the C5 p sweep (BASELINE.json configs[4]; reference sweep_p,
+    pipeline.py:465-498): µs/layer at this p and the per-head budget skew --
+    B1 per head split into focused (tau 0.25) and diffuse (tau 2.0) heads."""
+    old = [d.params.p for d in decs]
+    for d in decs:
+        d.params.p = p
+    graphs = []
+    for i in range(len(decs)):
+        decs[i].step(q, k_new, v_new, positions, out)
+    torch.cuda.synchronize()
+    for i in range(len(decs)):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            decs[i].step(q, k_new, v_new, positions, out)
+        graphs.append(g)
+    for i in range(args.warmup):
+        graphs[i % len(decs)].replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        graphs[i % len(decs)].replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    st = decs[(args.steps - 1) % len(decs)].stats()
+    b1 = st.b1.float().cpu()
+    taus = torch.tensor(head_taus(cfg, decs[0].cache.num_kv_heads, int(os.environ.get("RANK", "0")), world))
+    def summ(x):
+        x = x.sort().values
+        return {"min": int(x[0]), "p50": int(x[len(x) // 2]), "max": int(x[-1]), "mean": round(float(x.mean()), 1)}
+    foc, dif = b1[taus == min(TAUS)], b1[taus == max(TAUS)]
+    for d, v in zip(decs, old):
+        d.params.p = v
+    return {"p": p, "us_per_layer": round(ms * 1e3, 2), "head_b1": summ(b1),
+            "focused_b1 (tau 0.25)": summ(foc), "diffuse_b1 (tau 2.0)": summ(dif),
+            "skew_diffuse_over_focused_mean": round(float(dif.mean() / max(foc.mean(), 1.0)), 1),
+            "group_final_tokens_mean": round(float(st.group_b1.float().mean()), 1),
+            "candidate_mass_mean": round(float(st.candidate_mass.float().mean()), 6)}
+
+
 def run_ours(args, cfg):
     from paper_2502_02770_b200.decode import DecodeBuffers, PagedKVCache, TwilightDecoder, pages_for
     from paper_2502_02770_b200.workload import make_batch, tau_schedule
@@ -279,14 +341,14 @@ def run_ours(args, cfg):
     out = torch.empty(B, H_local * G, 128, dtype=torch.float32, device=dev)
     gathered = torch.empty(world * B, H_local * G, 128, dtype=torch.float32, device=dev) if (
         cfg["shard"] == "head" and world > 1) else None
+    full_out = torch.empty(B, world * H_local * G, 128, dtype=torch.float32, device=dev) if gathered is not None \
+        else None
 
-    def step_once(i, which=None):
-        dec = decs[i % L]
-        if which is None:
-            dec.step(q, k_new, v_new, positions, out)
-        if gathered is not None:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(gathered, out)
+    def gather():
+        # head-sharded (C3): the step ends with the all-gather of the per-rank heads, permuted
+        # back to head order (dist.gather_head_outputs)
+        from paper_2502_02770_b200.dist import gather_head_outputs
+        gather_head_outputs(out, world, buf=gathered, out=full_out)
 
     # --- CUDA graphs: one graph per layer for the fused step (launch-bound otherwise)
     graphs = []
@@ -307,8 +369,7 @@ def run_ours(args, cfg):
     def replay(i):
         graphs[i % L].replay()
         if gathered is not None:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(gathered, out)
+            gather()
 
     for i in range(args.warmup):
         replay(i)
@@ -329,7 +390,12 @@ def run_ours(args, cfg):
         barrier(world)
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms_local, world)
+    ms_min = min_over_ranks(ms_local, world)  # per-rank imbalance (head sharding: budget skew across heads)
     clocks = clk.summary()
+
+    # --- p sweep (C5): the same caches, one graph set per p, K timed steps each
+    p_list = [float(x) for x in args.p.split(",")] if args.p else list(cfg.get("p_sweep", ()))
+    sweep = [sweep_point(args, cfg, decs, q, k_new, v_new, positions, out, p, world) for p in p_list] if p_list else None
 
     # --- per-stage breakdown: each stage captured in its own CUDA graph, events between replays
     stage_ms = stage_breakdown(decs, q, k_new, v_new, positions, out, reps=max(3, min(args.steps, 10)))
@@ -362,7 +428,8 @@ def run_ours(args, cfg):
     q_d = inp_d[:nq].view(q.shape)
     k_d = inp_d[nq:nq + nk].view(k_new.shape)
     v_d = inp_d[nq + nk:].view(v_new.shape)
-    out_h = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    res_src = full_out if full_out is not None else out  # the step's result: all heads after the gather
+    out_h = torch.empty(res_src.shape, dtype=res_src.dtype).pin_memory()
     # single GPU: the H2D copy, the step and the D2H copy are captured as ONE graph
     # (memcpy nodes from/to the pinned buffers, executed every replay)
     copies_in_graph = gathered is None
@@ -388,15 +455,14 @@ def run_ours(args, cfg):
             inp_d.copy_(inp_h, non_blocking=True)
         e2e_graphs[i % L].replay()
         if gathered is not None:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(gathered, out)
+            gather()
         if not copies_in_graph:
-            out_h.copy_(out, non_blocking=True)
+            out_h.copy_(res_src, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
     h2d = q.numel() * q.element_size() + k_new.numel() * k_new.element_size() * 2
-    d2h = out.numel() * out.element_size()
+    d2h = res_src.numel() * res_src.element_size()
 
     # --- bytes, roofline, stats
     dec0 = decs[(args.steps - 1) % L]
@@ -458,6 +524,7 @@ def run_ours(args, cfg):
                                  "batch); its HBM fraction is not the limiter"}
                         if dominant in ("K2_select", "K3bc_topp") and kernel_gbs[dominant]
                         and kernel_gbs[dominant] / peak < 0.2 else {})},
+        "rank_ms": {"min": round(ms_min, 5), "max": round(ms, 5)},
         "step_roofline": {"algorithmic_bytes": ab["step"], "achieved_gbs_per_gpu": round(achieved_step, 1),
                           "frac": round(achieved_step / peak, 4)},
         "kernels_us": {k: round(v * 1e3, 2) for k, v in stage_ms.items()},
@@ -472,6 +539,8 @@ def run_ours(args, cfg):
                     "head_b1_mean": round(float(b1.mean().item()), 1)},
         "clocks": clocks,
     }
+    if sweep:
+        res["p_sweep"] = sweep
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(cfg, n, samples=args.cpu_units)
     if world > 1:
@@ -733,10 +802,89 @@ def cpu_baseline(cfg, n, samples=8):
             "seconds_per_unit": round(per_unit, 4)}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")  # nucleuskv, pip-installed --target (git-ignored, travels)
+_REF_UNITS = []
+
+
+def _ref_pkg_available() -> bool:
+    if not os.path.isdir(os.path.join(REF_PKG, "nucleuskv")):
+        return False
+    if REF_PKG not in sys.path:
+        sys.path.insert(0, REF_PKG)
+    try:
+        import nucleuskv.pipeline  # noqa: F401
+        return True
+    except Exception:
+        return False
+
+
+def _ref_build_unit(cfg, n, i, with_pkg):
+    """Unit i of the reference arm: KV head h = i (tau = TAUS[h % 4], the GPU
+    arm's mix), its cache prebuilt by the oracle and (when installed) by the
+    reference package itself (pipeline.py:177-201 with cache=/metadata=)."""
+    from oracle import twilight_oracle as orc
+    K, V, Q = _unit_arrays(cfg, n, i, 100 + i)
+    unit = {"K": K, "V": V, "Q": Q, "prep": orc.prepare_unit(K)}
+    if with_pkg:
+        from nucleuskv import pipeline as P, quantcache as QC, selectors as S
+        from nucleuskv.pruner import BinarySearchConfig
+        sel = S.SelectorConfig(kind="quest", budget=int(cfg["budget"])) if cfg["selector"] == "quest" else \
+            S.SelectorConfig(kind="full")
+        unit["pcfg"] = P.PipelineConfig(selector=sel, prune=BinarySearchConfig(p=cfg["p"]), estimator_bits=4,
+                                        group_map=S.GroupMap(cfg["G"]))
+        unit["cache"], unit["meta"] = QC.build_cache(K, page_size=16, bits=4)
+    return unit
+
+
+def _ref_task(args):
+    """One step's share of one worker: unit i through the oracle port (always)
+    or through nucleuskv's own run_grouped / run_head with the prebuilt cache."""
+    i, which = args
+    cfg, n = _POOL_STATE["cfg"], _POOL_STATE["n"]
+    u = _REF_UNITS[i]
+    t0 = time.perf_counter()
+    if which == "port":
+        _cpu_unit((cfg, n, i, 0, (u["K"], u["V"], u["Q"], u["prep"])))
+    else:
+        from nucleuskv import pipeline as P
+        if cfg["G"] == 1:
+            P.run_head(u["Q"][0], u["K"], u["V"], u["pcfg"], cache=u["cache"], metadata=u["meta"])
+        else:
+            P.run_grouped(u["Q"], u["K"], u["V"], u["pcfg"], cache=u["cache"], metadata=u["meta"])
+    return time.perf_counter() - t0
+
+
+def _ref_worker_init():
+    os.environ["OMP_NUM_THREADS"] = "1"
+    try:  # one BLAS thread per worker process (BLAS was initialised in the parent)
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+
+
 def run_reference(args, cfg):
-    """--impl reference: the reference algorithm (oracle port; the reference
-    is pure Python and cannot be compiled into oracle/_ref) on all host cores,
-    rank 0 only; each step = one unit per worker, extrapolated to the batch."""
+    """--impl reference: the reference's own CPU path on all host cores, rank 0
+    only.  Each step runs `width` (sequence, KV head) units in parallel, one
+    per worker process, covering the GPU arm's tau mix, with every cache
+    prebuilt (the GPU arm's step appends into a prebuilt cache too):
+      * nucleuskv itself (the reference package, pip-installed into
+        baseline/_ref) through run_grouped / run_head -- the line's value;
+      * the NumPy restatement in oracle/ (hot path only, no report work) --
+        reported beside it.
+    ms_per_step is the measured wall of one step (the sample); value is that
+    wall extrapolated to the whole batch (x units / width)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -745,27 +893,51 @@ def run_reference(args, cfg):
     n = cfg["n"]
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     H_local = cfg["H"] // world if cfg["shard"] == "head" else cfg["H"]
+    cfg = dict(cfg, H_local=H_local)
     units = cfg["B"] * H_local * (world if cfg["shard"] == "batch" and not cfg.get("model") else 1)
+    width = max(1, min(cores, 16 if n > 65536 else 32, units))
+    with_pkg = _ref_pkg_available()
+    _POOL_STATE["cfg"], _POOL_STATE["n"] = cfg, n
+    _REF_UNITS.clear()
+    for i in range(width):  # built in the parent, shared copy-on-write by the forked workers
+        _REF_UNITS.append(_ref_build_unit(cfg, n, i, with_pkg))
+    legs = {}
     ctx = mp.get_context("fork")
-    with ctx.Pool(cores, initializer=_pool_init, initargs=(cfg, n, 4242)) as pool:
-        for _ in range(args.warmup):
-            pool.map(_pool_task, range(cores))
-        walls = []
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            pool.map(_pool_task, range(cores))
-            walls.append(time.perf_counter() - t0)
-    per_step = statistics.mean(walls) * units / cores  # seconds for the whole layer
-    value = round(per_step * 1e6, 1)
-    res = {"metric": METRIC, "value": value, "unit": "us/layer", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(per_step * 1e3, 3), "higher_is_better": False,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (NumPy)", "data": "synthetic, seeded",
+    with ctx.Pool(width, initializer=_ref_worker_init) as pool:
+        for which in (["pkg"] if with_pkg else []) + ["port"]:
+            steps = args.steps if which == "port" else max(1, min(args.steps, 5))
+            for _ in range(1 if which == "pkg" else args.warmup):
+                pool.map(_ref_task, [(i, which) for i in range(width)], chunksize=1)
+            walls, per_unit = [], []
+            for _ in range(steps):
+                t0 = time.perf_counter()
+                per_unit += pool.map(_ref_task, [(i, which) for i in range(width)], chunksize=1)
+                walls.append(time.perf_counter() - t0)
+            wall = statistics.mean(walls)
+            legs[which] = {"ms_per_step": round(wall * 1e3, 3), "steps": steps,
+                           "value": round(wall * units / width * 1e6, 1),
+                           "seconds_per_unit": round(statistics.mean(per_unit), 4)}
+    main_leg = "pkg" if with_pkg else "port"
+    L = legs[main_leg]
+    kind = "reference" if with_pkg else "port"
+    what = ("nucleuskv (the reference package, baseline/_ref) run_grouped/run_head with prebuilt cache" if with_pkg
+            else "oracle/twilight_oracle.py (NumPy restatement of nucleuskv)")
+    res = {"metric": METRIC, "value": L["value"], "unit": "us/layer", "n_gpus": world, "steps": L["steps"],
+           "warmup": args.warmup, "ms_per_step": L["ms_per_step"], "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (NumPy)",
+           "data": "synthetic, seeded (NumPy): the GPU arm's shapes and per-KV-head tau mix",
            "impl": "reference",
            "config": {"workload": cfg["desc"], "config_id": args.config},
-           "cpu_baseline": {"value": value, "unit": "us/layer", "cores": cores, "kind": "port",
-                            "sample": f"each step: {cores} (sequence, kv-head) units at ctx {n} in parallel "
-                                      f"(one per core), extrapolated to {units} units"},
-           "e2e": {"value": value, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "extrapolation": {"units_per_layer": units, "units_per_step": width, "factor": round(units / width, 3),
+                             "note": "ms_per_step = measured wall of one step (width units in parallel); "
+                                     "value = that wall x factor"},
+           "cpu": {"model": cpu_model(), "cores_available": cores},
+           "cpu_baseline": {"value": L["value"], "unit": "us/layer", "cores": width, "kind": kind,
+                            "sample": f"each step: {width} (sequence, kv-head) units at ctx {n} in parallel (one "
+                                      f"per core, tau mix {TAUS}), {what}; extrapolated x{units / width:.2f} to "
+                                      f"{units} units"},
+           "legs": legs,
+           "e2e": {"value": L["value"], "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(res), flush=True)
 
 
@@ -779,6 +951,7 @@ def main():
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--waves", type=int, default=1, help="sub-batches pipelined on separate streams (1 = off; measured slower at C2)")
     ap.add_argument("--cpu-units", type=int, default=8)
+    ap.add_argument("--p", default="", help="comma-separated top-p sweep (default: the config's own, C5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

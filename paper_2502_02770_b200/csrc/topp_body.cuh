@@ -22,6 +22,10 @@ static __device__ unsigned long long g_tt[1024][8];
 #endif
 
 constexpr int kBins = TW_TOPP_BINS;      // 4096
+// per-head histograms are stored with one pad word per 16 bins, so the crossing
+// scan's threads (16 consecutive bins each) read different banks
+constexpr int kBinsP = kBins + kBins / 16;
+__device__ __forceinline__ int hidx(int b) { return b + (b >> 4); }
 constexpr float kBinPerLogit = 120.0f;   // bins cover (max - z) in [0, 34.1); the last bin takes the rest
 constexpr int kHB = 4;                   // heads whose histograms are resident at once (4 x 32 KB)
 constexpr int kMemberCap = TW_TOPP_MEMBER_CAP;
@@ -296,7 +300,7 @@ struct UnitCfg {
   static constexpr int GT = GTO ? GTO : G <= 2 ? 512 : 256;  // threads per head (warp group)
   static constexpr int NT = GT * GB;            // threads
   static constexpr int MC = HB >= kHB ? kMemberCap : kMemberCap / 2;  // member-list capacity
-  static constexpr size_t kHistBytes = (size_t)GB * kBins * 8;
+  static constexpr size_t kHistBytes = (size_t)GB * kBinsP * 8;
   static constexpr size_t kResBytes = (size_t)GB * sizeof(ResGroupSmem);
   static constexpr size_t kSmem = (kHistBytes > kResBytes ? kHistBytes : kResBytes) + (size_t)MC * 8;
   // the union bitmap lives in the histogram region (dead after the crossing
@@ -312,8 +316,8 @@ __device__ __forceinline__ void topp_unit_body(const int unit, const tw_paged_kv
   using Cfg = UnitCfg<G, HB, GTO>;
   constexpr int GB = Cfg::GB, NT = Cfg::NT, kGT = Cfg::GT, MC = Cfg::MC;
   constexpr int kPerT = kBins / kGT;  // bins per thread in the crossing scan
-  uint32_t* Hc = reinterpret_cast<uint32_t*>(sm);                           // [GB][kBins] counts
-  uint32_t* Hu = Hc + GB * kBins;                                            // [GB][kBins] deficit sums
+  uint32_t* Hc = reinterpret_cast<uint32_t*>(sm);                           // [GB][kBinsP] counts
+  uint32_t* Hu = Hc + GB * kBinsP;                                           // [GB][kBinsP] deficit sums
   ResGroupSmem* RS = reinterpret_cast<ResGroupSmem*>(sm);                    // [GB] (aliases the bins)
   uint32_t* mkey = reinterpret_cast<uint32_t*>(sm + Cfg::kSmem - (size_t)MC * 8);  // [MC]
   uint32_t* mpos = mkey + MC;                                                 // [MC]
@@ -352,7 +356,7 @@ __device__ __forceinline__ void topp_unit_body(const int unit, const tw_paged_kv
   // ---- pass 1 (per batch of GB heads): bins, then each head's crossing bin
 #pragma unroll 1
   for (int g0 = 0; g0 < G; g0 += GB) {
-    for (int i = tid; i < GB * kBins; i += NT) Hc[i] = Hu[i] = 0;
+    for (int i = tid; i < GB * kBinsP; i += NT) Hc[i] = Hu[i] = 0;
     if (tid < GB) s_deep[tid] = 0;
     __syncthreads();
     {
@@ -380,8 +384,8 @@ __device__ __forceinline__ void topp_unit_body(const int unit, const tw_paged_kv
             if (z > -INFINITY) {
               const int b = dbin(z, m120[h]);
               const uint32_t d = deficit(z, Mh[h], b);
-              atomicAdd(&Hc[h * kBins + b], 1u);
-              if (b < kBins - 1) atomicAdd(&Hu[h * kBins + b], d);
+              atomicAdd(&Hc[h * kBinsP + hidx(b)], 1u);
+              if (b < kBins - 1) atomicAdd(&Hu[h * kBinsP + hidx(b)], d);
               else deep[h] += d;  // the deepest bin's deficits (up to 2^22 each) need 64 bits
             }
           }
@@ -397,8 +401,8 @@ __device__ __forceinline__ void topp_unit_body(const int unit, const tw_paged_kv
     TT(1);
     const int g = g0 + gp;
     if (g < G && R[g].cb != -2) {  // uniform per warp group
-      const uint32_t* hc = Hc + gp * kBins;
-      const uint32_t* hu = Hu + gp * kBins;
+      const uint32_t* hc = Hc + gp * kBinsP;
+      const uint32_t* hu = Hu + gp * kBinsP;
       const float M = R[g].M;
       const float M120 = M * kBinPerLogit;
       const int bfirst = grp.tid * kPerT;
@@ -412,9 +416,9 @@ __device__ __forceinline__ void topp_unit_body(const int unit, const tw_paged_kv
 #endif
       auto mass = [&](int i, uint32_t& c) -> double {
         const int bb = bfirst + i;
-        c = hc[bb];
+        c = hc[hidx(bb)];
         if (!c) return 0.0;
-        const uint64_t us = bb == kBins - 1 ? (uint64_t)s_deep[gp] : (uint64_t)hu[bb];
+        const uint64_t us = bb == kBins - 1 ? (uint64_t)s_deep[gp] : (uint64_t)hu[hidx(bb)];
         // exp(t_b - M) = w0 * exp(t_b - t0);  t_b - t0 = -i/120 + d (d ~ float rounding, tiny)
         const float d = (bin_top(M, bb) - t0) + (float)i * (1.0f / 120.0f);
         const float w = w0 * kStepExpF[i] * (1.0f + d);

@@ -54,6 +54,15 @@ extern "C" int tw_debug_unit_ttrace(unsigned long long* host_out) {  // the top-
   cudaMemcpyToSymbol(tw::g_tt, zeros, sizeof(zeros));
   return 0;
 }
+extern "C" int tw_debug_unit_strace(unsigned long long* host_out) {  // the select body's phase stamps
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host_out, g_strace, sizeof(g_strace));
+  int zeros[512] = {0};
+  cudaMemcpyToSymbol(g_strace_phase, zeros, sizeof(zeros));
+  static unsigned long long z2[512 * 16];
+  cudaMemcpyToSymbol(g_strace, z2, sizeof(z2));
+  return 0;
+}
 #endif
 
 namespace tw {
@@ -369,8 +378,8 @@ static int unit_min_units() {
 // 1 when the fused per-unit kernel covers this step's geometry and options.
 int tw_unit_step_applies(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_buffers* buf,
                          const int32_t* positions) {
-  const char* e = getenv("TW_UNIT");
-  if (e && atoi(e) == 0) return 0;
+  const char* e = getenv("TW_UNIT");  // opt-in until it beats the separate kernels at every config
+  if (!e || atoi(e) == 0) return 0;
   if (!kv || !prm || !buf || kv->dtype != TW_BF16 || kv->head_dim != kHeadDim || (kv->bits != 0 && kv->bits != 4))
     return 0;
   if (prm->estimator != TW_ESTIMATE_INT || prm->renormalize != 1) return 0;

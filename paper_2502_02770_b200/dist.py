@@ -49,20 +49,28 @@ def local_queries(q: torch.Tensor, H_kv: int, G: int, world: int, rank: int, mod
     raise ValueError(mode)
 
 
-def gather_head_outputs(out_local: torch.Tensor, world: int, group=None) -> torch.Tensor:
+def gather_head_outputs(out_local: torch.Tensor, world: int, group=None, buf: torch.Tensor | None = None,
+                        out: torch.Tensor | None = None) -> torch.Tensor:
     """All-gather per-rank outputs [B, Hq/N, d] into [B, Hq, d] (head-sharded mode).
 
-    One collective (all_gather_into_tensor) of world * B*Hq/N*d floats; the
-    rank-major result is permuted back to head order.
+    One collective (all_gather_into_tensor) of world * B*Hq/N*d floats into
+    `buf` [N*B, Hq/N, d]; the rank-major result is permuted back to head order
+    (into `out` [B, Hq, d] when given).  Pre-allocated buffers keep the step
+    allocation-free.
     """
     import torch.distributed as dist
 
     if world == 1:
         return out_local
     B, hq_local, d = out_local.shape
-    buf = torch.empty(world * B, hq_local, d, dtype=out_local.dtype, device=out_local.device)
+    if buf is None:
+        buf = torch.empty(world * B, hq_local, d, dtype=out_local.dtype, device=out_local.device)
     dist.all_gather_into_tensor(buf, out_local.contiguous(), group=group)
-    return buf.view(world, B, hq_local, d).permute(1, 0, 2, 3).reshape(B, world * hq_local, d)
+    full = buf.view(world, B, hq_local, d).permute(1, 0, 2, 3)
+    if out is None:
+        return full.reshape(B, world * hq_local, d)
+    out.view(B, world, hq_local, d).copy_(full)
+    return out
 
 
 def gather_batch_outputs(out_local: torch.Tensor, world: int, group=None) -> torch.Tensor:

@@ -55,6 +55,7 @@ def _same(a, b, what):
     dict(B=16, H=8, G=4, n=4100, selector="quest", budget=1024, p=0.0),        # p = 0: nothing kept
     dict(B=16, H=8, G=4, n=4100, selector="quest", budget=1024, p=0.95, ragged=True),
     dict(B=16, H=4, G=1, n=3000, selector="full", budget=None, p=0.95, ragged=True, aliased=True),
+    dict(B=16, H=8, G=4, n=32767, selector="quest", budget=8192, p=0.95),      # the C2 bench geometry
 ])
 def test_unit_kernel_matches_separate_kernels(case):
     case = dict(case)

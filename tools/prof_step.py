@@ -34,9 +34,12 @@ out = torch.empty(B, H * G, 128, device="cuda")
 from paper_2502_02770_b200 import _lib as _lib0  # noqa: E402
 for _ in range(args.reps):
     cache.append(batch.k_new, batch.v_new, pos)
-    dec.select(q)
-    dec.estimate(q)
-    dec.topp()
+    if dec.unit_path:
+        dec.select_estimate_topp(q)
+    else:
+        dec.select(q)
+        dec.estimate(q)
+        dec.topp()
     dec.attend(q, out)
     if args.dense:
         dec.dense(q, out)

@@ -13,8 +13,11 @@ for c in C1 C3 C5; do timeout 900 python bench.py --config $c --no-cpu-baseline 
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches_${TAG}_C2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 python tools/launches.py gpurun_out/launches_${TAG}_C2.csv --json gpurun_out/launches_${TAG}_C2.json | grep "tw::" || true
-timeout 900 ncu --set full --import-source on --clock-control none \
-  -k regex:"attn_kernel|quest_select|topp_unit|estimate_kernel|quest_filter|append_kernel|merge_kernel" -c 8 \
-  -o gpurun_out/full_${TAG}_C2 python tools/prof_step.py --config C2 --reps 1 > /dev/null 2>&1
-python tools/ncu_hot.py gpurun_out/full_${TAG}_C2.ncu-rep . --lines 6 > gpurun_out/ncu_full_${TAG}_C2.txt 2>&1
-python tools/traffic_json.py gpurun_out/full_${TAG}_C2.ncu-rep C2 > gpurun_out/traffic_${TAG}_C2.json 2>&1 || true
+for c in C1 C2 C3 C5; do
+  timeout 900 ncu --set full --import-source on --clock-control none \
+    -k regex:"attn_kernel|quest_select|topp_unit|topp_head|estimate_kernel|quest_filter|append_kernel|merge_kernel|unit_step" -c 8 \
+    -o gpurun_out/full_${TAG}_$c python tools/prof_step.py --config $c --reps 1 > /dev/null 2>&1
+  python tools/ncu_hot.py gpurun_out/full_${TAG}_$c.ncu-rep . --lines 6 > gpurun_out/ncu_full_${TAG}_$c.txt 2>&1
+  python tools/traffic_json.py gpurun_out/full_${TAG}_$c.ncu-rep $c > gpurun_out/traffic_${TAG}_$c.json 2>&1 || true
+done
+cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json

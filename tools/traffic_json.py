@@ -16,6 +16,7 @@ STAGES = {
     "K3a_estimate": ["estimate_kernel"],
     "K3bc_topp": ["topp_unit"],
     "K4_attention": ["attn_kernel", "merge_kernel"],
+    "K23_unit": ["unit_step"],
 }
 
 rep, cfg = sys.argv[1], sys.argv[2]

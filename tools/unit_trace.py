@@ -37,6 +37,7 @@ q = step.q.contiguous()
 buf = (ctypes.c_ulonglong * (4096 * 8))()
 res = {}
 tbuf = (ctypes.c_ulonglong * (1024 * 8))()
+sbuf = (ctypes.c_ulonglong * (512 * 16))()
 ttrace = hasattr(_lib.lib(), "tw_debug_unit_ttrace")
 utrace = hasattr(_lib.lib(), "tw_debug_utrace")  # absent in the normal build (e.g. under ncu)
 for rep in range(4):
@@ -46,6 +47,7 @@ for rep in range(4):
         _lib.lib().tw_debug_utrace(buf)
     if ttrace:
         _lib.lib().tw_debug_unit_ttrace(tbuf)
+        _lib.lib().tw_debug_unit_strace(sbuf)
 if not utrace:
     sys.exit(0)
 a = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 8).astype(np.int64)[:, :5]
@@ -64,6 +66,13 @@ if ttrace:  # top-p body stamps TT(0..5): start, pass 1, crossings, pass 2, reso
     tt = tt[(tt[:, :6] > 0).all(axis=1)]
     res["topp_phases"] = ["pass1", "crossing", "pass2", "resolve", "compaction"]
     res["topp_phase_mean_us"] = (np.diff(tt, axis=1) / 1e3).mean(axis=0).round(2).tolist()
+    tt8 = np.frombuffer(tbuf, dtype=np.uint64).reshape(1024, 8).astype(np.int64)
+    row = tt8[0]
+    res["topp_cta0_stamps_us"] = ((row - row[0]) / 1e3).round(2).tolist()  # slots 0..7 (6: crossing start, 7: crossing end, head group 0)
+    st = np.frombuffer(sbuf, dtype=np.uint64).reshape(512, 16).astype(np.int64)
+    st = st[st[:, 0] > 0]
+    k = int((st > 0).sum(axis=1).min())
+    res["select_phase_mean_us"] = (np.diff(st[:, :k], axis=1) / 1e3).mean(axis=0).round(2).tolist()
 print(json.dumps(res))
 if args.json:
     with open(args.json, "w") as f:
