@@ -1,5 +1,6 @@
 // Shared device helpers for the Twilight sm_100a kernels.
 #pragma once
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 
@@ -133,6 +134,7 @@ constexpr int TW_FUSE_UNAVAILABLE = -1;
 
 inline int launch_status() {
   cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && getenv("TW_DEBUG")) fprintf(stderr, "twilight: CUDA error %s\n", cudaGetErrorString(e));
   return e == cudaSuccess ? TW_OK : TW_ERR_CUDA;
 }
 

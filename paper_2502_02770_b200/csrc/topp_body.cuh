@@ -55,18 +55,33 @@ __device__ __forceinline__ int dbin(float z, float M120) {
 }
 __device__ __forceinline__ float bin_top(float M, int b) { return fmaf(-(float)b, 1.0f / kBinPerLogit, M); }
 // Largest float z with dbin(z) >= b (dbin is non-increasing in z), so bin b
-// is the float interval (bin_ceiling(b + 1), bin_ceiling(b)].
+// is the float interval (bin_ceiling(b + 1), bin_ceiling(b)].  The guess
+// M - b/120 is off by the rounding of M120 (~|M| 3e-8 absolute), which near
+// z = 0 is hundreds of ulps, so the exact boundary is found by bisection over
+// the ordered float keys of a bracket much wider than that error and much
+// narrower than a bin.
 static __device__ __noinline__ float bin_ceiling(int b, float M, float M120) {
   if (b <= 0) return INFINITY;
   if (b >= kBins) return -INFINITY;
-  float e = M - (float)b / kBinPerLogit;
-  for (int i = 0; i < 64 && dbin(e, M120) < b; ++i) e = nextafterf(e, -INFINITY);
+  const float e = M - (float)b / kBinPerLogit;
+#ifdef TW_OLD_BIN_CEILING  // the round-1 64-ulp walk, kept only to show the regression test catches it
+  float x = e;
+  for (int i = 0; i < 64 && dbin(x, M120) < b; ++i) x = nextafterf(x, -INFINITY);
   for (int i = 0; i < 64; ++i) {
-    const float up = nextafterf(e, INFINITY);
+    const float up = nextafterf(x, INFINITY);
     if (dbin(up, M120) < b) break;
-    e = up;
+    x = up;
   }
-  return e;
+  return x;
+#endif
+  const float d = 2e-3f;  // a quarter bin
+  uint32_t lo = f2key(e - d), hi = f2key(e + d);  // dbin(lo) >= b > dbin(hi)
+  while (hi - lo > 1) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    if (dbin(key2f(mid), M120) >= b) lo = mid;
+    else hi = mid;
+  }
+  return key2f(lo);
 }
 __device__ __forceinline__ uint32_t deficit(float z, float M, int b) {
   const float r = ex2_approx((z - bin_top(M, b)) * 1.4426950408889634f);
@@ -529,6 +544,11 @@ __device__ __forceinline__ void topp_unit_body(const int unit, const tw_paged_kv
     }
   }
   __syncthreads();
+#ifdef TW_TOPP_CHECK
+  if (tid < G && R[tid].seg >= 0 && s_fill[tid] != (int)R[tid].members)
+    printf("topp member mismatch unit %d head %d counted %u listed %d cb %d M %a zhi %a zlo %a\n", unit, tid,
+           R[tid].members, s_fill[tid], R[tid].cb, R[tid].M, R[tid].zhi, R[tid].zlo);
+#endif
 
   TT(3);
   // ---- resolve: exact threshold class inside each head's crossing bin (warp group per head)
@@ -549,6 +569,11 @@ __device__ __forceinline__ void topp_unit_body(const int unit, const tw_paged_kv
       uint32_t c = 0;
       unsigned long long us = 0;
       auto pick = [&](uint32_t k, uint32_t u, uint32_t pos) {
+#ifdef TW_TOPP_CHECK
+        if (pos >= (uint32_t)npos)
+          printf("topp bad pos unit %d head %d pos %u npos %d seg %d members %u MC %d\n", unit, g, pos, npos, h.seg,
+                 h.members, MC);
+#endif
         if (k >= thr) {
           ++c;
           us += u;

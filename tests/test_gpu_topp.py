@@ -154,3 +154,25 @@ def test_topp_more_units_than_sms():
     npages = [int(x) for x in rng.integers(1, T // 16 + 1, size=U)]
     dec = run_topp(z, npages, 0.9)
     check(dec, z, npages, 0.9)
+
+
+@pytest.mark.parametrize("p", [0.2, 0.4, 0.6, 0.8])
+def test_topp_bin_boundaries_near_zero(p):
+    """Crossing bins whose edges lie near z = 0, where the float guess
+    M - b/120 is hundreds of ulps from the exact edge of dbin's bin (the
+    rounding of M*120 is ~|M| 3e-8 absolute, the ulp of z ~1e-9): a dense
+    cloud of logits on both sides of the edges of the bins around zero, so
+    the pass-2 membership interval must equal pass 1's binning exactly (a
+    mismatch corrupted the member list on C5 at p = 0.85)."""
+    M = np.float32(4.1929)
+    vals = [M]
+    for b in (504, 505, 506):  # edges at z ~ -0.007, -0.015, -0.024 (M * 120 ~ 503.1)
+        e = np.float32(M - np.float32(b) / np.float32(120.0))
+        for k in range(-900, 901, 5):
+            vals.append(np.float32(e + np.float32(k) * np.spacing(e)))
+    v = np.unique(np.asarray(vals, dtype=np.float32))
+    z = np.full((1, 1, 16 * (-(-v.size // 16))), -np.inf, dtype=np.float32)
+    z[0, 0, : v.size] = np.random.default_rng(3).permutation(v)
+    npages = [z.shape[2] // 16]
+    dec = run_topp(z, npages, p)
+    check(dec, z, npages, p)
