@@ -330,7 +330,8 @@ def run_ours(args, cfg):
         cache.prefill(batch.K[:, :, : n - 1], batch.V[:, :, : n - 1])  # the step appends token n-1
         del batch
         dec = TwilightDecoder(cache, cfg["selector"], budget=cfg["budget"], p=cfg["p"], bufs=shared,
-                              waves=args.waves if B % max(args.waves, 1) == 0 else 1)
+                              waves=args.waves if B % max(args.waves, 1) == 0 else 1,
+                              chunk_tokens=args.chunk or None)
         shared = dec.bufs
         caches.append(cache)
         decs.append(dec)
@@ -951,6 +952,7 @@ def main():
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--waves", type=int, default=1, help="sub-batches pipelined on separate streams (1 = off; measured slower at C2)")
     ap.add_argument("--cpu-units", type=int, default=8)
+    ap.add_argument("--chunk", type=int, default=0, help="attention work-item tokens (0: auto)")
     ap.add_argument("--p", default="", help="comma-separated top-p sweep (default: the config's own, C5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

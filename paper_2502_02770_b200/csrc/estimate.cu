@@ -40,7 +40,9 @@ constexpr int kEstStages = TW_EST_STAGES;  // pages in flight per warp (cp.async
 
 // Persistent warp workers over (unit, 32-candidate-page) items, chunk-major;
 // each warp streams its pages' 1152-B INT4 blocks through a 4-deep cp.async ring.
-template <typename T, int G, int BITS>
+// MASKED: the sink-window or channel-pruned selectors' token masks are
+// applied; the plain (Quest / full) variant drops those per-page tests.
+template <typename T, int G, int BITS, bool MASKED>
 __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv, const T* __restrict__ q,
                                                                   tw_decode_buffers buf, int max_chunks,
                                                                   int sw_sink, int sw_window,
@@ -194,10 +196,13 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       }
       const int tok_r = lp * kPage + r;
       // sink-window selection (selectors.py:164-175): tokens between the sink and the window are not candidates
-      const bool swm = sw_window >= 0 && sw_sink + sw_window < n;
-      bool v_r = tok_r < n && (!swm || tok_r < sw_sink || tok_r >= n - sw_window);
-      bool v_r8 = tok_r + 8 < n && (!swm || tok_r + 8 < sw_sink || tok_r + 8 >= n - sw_window);
-      if (tok_mask) {  // channel-pruned selection: only the selected tokens of a candidate page
+      bool v_r = tok_r < n, v_r8 = tok_r + 8 < n;
+      if constexpr (MASKED) {
+        const bool swm = sw_window >= 0 && sw_sink + sw_window < n;
+        v_r = v_r && (!swm || tok_r < sw_sink || tok_r >= n - sw_window);
+        v_r8 = v_r8 && (!swm || tok_r + 8 < sw_sink || tok_r + 8 >= n - sw_window);
+      }
+      if (MASKED && tok_mask) {  // channel-pruned selection: only the selected tokens of a candidate page
         const uint32_t mw = __ldg(tok_mask + (size_t)unit * ((T_stride + 31) / 32) + (tok_r >> 5));
         v_r = v_r && ((mw >> (tok_r & 31)) & 1u);
         v_r8 = v_r8 && ((mw >> ((tok_r + 8) & 31)) & 1u);
@@ -355,7 +360,7 @@ static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, estimate_kernel<T, G, BITS>, kEstWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, estimate_kernel<T, G, BITS, false>, kEstWarps * 32, 0);
   int grid = sms * persist_cap(per_sm);
   // item size: 32 pages (amortises the per-item index lookups and ring fill) unless
   // that leaves warps idle -- small batches split into 16-, 8- or 4-page items
@@ -365,8 +370,12 @@ static void launch_estimate_g(const tw_paged_kv* kv, const T* q, const tw_decode
   const int max_chunks = (kv->max_pages + item - 1) / item;
   const int items = units * max_chunks;
   if (grid * kEstWarps > items) grid = (items + kEstWarps - 1) / kEstWarps;
-  launch_pdl(estimate_kernel<T, G, BITS>, dim3(grid), dim3(kEstWarps * 32), 0, stream, *kv, q, *buf, max_chunks, sw_sink,
-             sw_window, tok_mask, item);
+  if (sw_window >= 0 || tok_mask)
+    launch_pdl(estimate_kernel<T, G, BITS, true>, dim3(grid), dim3(kEstWarps * 32), 0, stream, *kv, q, *buf,
+               max_chunks, sw_sink, sw_window, tok_mask, item);
+  else
+    launch_pdl(estimate_kernel<T, G, BITS, false>, dim3(grid), dim3(kEstWarps * 32), 0, stream, *kv, q, *buf,
+               max_chunks, sw_sink, sw_window, tok_mask, item);
 }
 
 template <typename T>

@@ -135,10 +135,17 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_kernel(tw_paged_kv
 // (bf16 products exact, fp32 accumulation, covered by the select margin).
 // Per warp: 16-page tiles (16 x 512 B, XOR-swizzled rows) through a TW_QM_STAGES-deep (2)
 // cp.async ring; one ldmatrix.x4 + one MMA per page-tile k-step.
+// TW_QM_TILE = 8: 8-page tiles with the MMA roles swapped (the G query rows are
+// the A operand, the tile's pages the N = 8 columns), so the same 16 KB per
+// warp holds 4 stages -- 3 tiles (12 KB) in flight instead of one 8 KB tile.
+#ifndef TW_QM_TILE
+#define TW_QM_TILE 16
+#endif
 #ifndef TW_QM_STAGES
-#define TW_QM_STAGES 2
+#define TW_QM_STAGES (TW_QM_TILE == 8 ? 4 : 2)
 #endif
 constexpr int kQmStages = TW_QM_STAGES;
+constexpr int kQmTile = TW_QM_TILE;  // pages per stage: 16 (pages = MMA rows) or 8 (pages = MMA columns)
 
 __device__ __forceinline__ void ldsm_x4_q(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -170,7 +177,8 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane & 3, r = lane >> 2, q8 = lane >> 3, rr = lane & 7;
   const int units = kv.num_seqs * kv.num_kv_heads;
-  uint8_t (*R)[16 * 512] = reinterpret_cast<uint8_t (*)[16 * 512]>(qm_ring + (size_t)warp * kQmStages * 16 * 512);
+  uint8_t (*R)[kQmTile * 512] =
+      reinterpret_cast<uint8_t (*)[kQmTile * 512]>(qm_ring + (size_t)warp * kQmStages * kQmTile * 512);
   uint32_t qb[16][2];  // B fragments of [qneg ; qpos] for head column r
   int cur_unit = -1;
   for (int it = warp_fetch(ctr); it < units * max_chunks; it = warp_fetch(ctr)) {
@@ -199,12 +207,12 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
     const uint8_t* src1 = base;
     if (lane < np) src0 += ((size_t)pt[p0 + lane] * kv.num_kv_heads + h) * 512;
     if (lane + 32 < np) src1 += ((size_t)pt[p0 + 32 + lane] * kv.num_kv_heads + h) * 512;
-    const int ntile = (np + 15) / 16;
+    const int ntile = (np + kQmTile - 1) / kQmTile;
     auto issue = [&](int s) {
       uint8_t* dst = R[s % kQmStages];
 #pragma unroll 4
-      for (int i = 0; i < 16; ++i) {
-        const int pg = 16 * s + i;
+      for (int i = 0; i < kQmTile; ++i) {
+        const int pg = kQmTile * s + i;
         if (pg < np) {
           const uint8_t* src = reinterpret_cast<const uint8_t*>(
               __shfl_sync(0xffffffffu, (unsigned long long)(pg < 32 ? src0 : src1), pg & 31));
@@ -248,21 +256,44 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
       __syncwarp();
       const uint8_t* tile = R[s % kQmStages];
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      const int row = (q8 & 1) * 8 + rr;
+      if constexpr (kQmTile == 16) {
+        const int row = (q8 & 1) * 8 + rr;
 #pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        uint32_t a[4];
-        const int chunk = 2 * kk + (q8 >> 1);
-        ldsm_x4_q(a, tile + row * 512 + ((chunk ^ (row & 7)) << 4));
-        mma_bf16_q(acc, a, qb[kk][0], qb[kk][1]);
-      }
-      __syncwarp();
-      // rows r, r+8 (pages), cols 2t, 2t+1 (heads)
+        for (int kk = 0; kk < 16; ++kk) {
+          uint32_t a[4];
+          const int chunk = 2 * kk + (q8 >> 1);
+          ldsm_x4_q(a, tile + row * 512 + ((chunk ^ (row & 7)) << 4));
+          mma_bf16_q(acc, a, qb[kk][0], qb[kk][1]);
+        }
+        __syncwarp();
+        // rows r, r+8 (pages), cols 2t, 2t+1 (heads)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int pg = 16 * s + r + (e >= 2 ? 8 : 0);
-        const int g = 2 * t + (e & 1);
-        if (g < G && pg < np) scores[((size_t)unit * G + g) * kv.max_pages + p0 + pg] = acc[e];
+        for (int e = 0; e < 4; ++e) {
+          const int pg = 16 * s + r + (e >= 2 ? 8 : 0);
+          const int g = 2 * t + (e & 1);
+          if (g < G && pg < np) scores[((size_t)unit * G + g) * kv.max_pages + p0 + pg] = acc[e];
+        }
+      } else {
+        // A = the q fragments (row r = head r, rows >= 8 zero: the same registers as the
+        // B fragments above), B = 8 page rows: ldmatrix matrix q8 = chunk 4kk2 + q8, row rr = page
+#pragma unroll
+        for (int kk2 = 0; kk2 < 8; ++kk2) {
+          uint32_t bf[4];
+          const int chunk = 4 * kk2 + q8;
+          ldsm_x4_q(bf, tile + rr * 512 + ((chunk ^ rr) << 4));
+          const uint32_t a0[4] = {qb[2 * kk2][0], 0u, qb[2 * kk2][1], 0u};
+          const uint32_t a1[4] = {qb[2 * kk2 + 1][0], 0u, qb[2 * kk2 + 1][1], 0u};
+          mma_bf16_q(acc, a0, bf[0], bf[1]);
+          mma_bf16_q(acc, a1, bf[2], bf[3]);
+        }
+        __syncwarp();
+        // row r (head), cols 2t, 2t+1 (pages)
+        if (r < G) {
+          const int pg = 8 * s + 2 * t;
+          float* so = scores + ((size_t)unit * G + r) * kv.max_pages + p0;
+          if (pg < np) so[pg] = acc[0];
+          if (pg + 1 < np) so[pg + 1] = acc[1];
+        }
       }
     }
     cp_wait<0>();
@@ -332,7 +363,7 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
     };
     if constexpr (sizeof(T) == 2) {
       auto gom = [&](auto kern) {
-        const int smem = kQfWarps * kQmStages * 16 * 512;
+        const int smem = kQfWarps * kQmStages * kQmTile * 512;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQfWarps * 32, smem);
@@ -372,9 +403,15 @@ int tw_select_channel_pruned(const tw_paged_kv* kv, const void* q, const tw_deco
 // step must append separately: fp32 cache, other selectors, a select kernel
 // that would not fit shared memory, or `positions` aliasing kv->seq_lens (the
 // filter writes seq_lens while later items still read their positions).
+int tw_unit_select(const tw_paged_kv* kv, const void* q, const void* k_new, const void* v_new,
+                   const int32_t* positions, const tw_decode_params* prm, const tw_decode_buffers* buf,
+                   cudaStream_t stream);  // unit.cu
+
 int tw_select_append(const tw_paged_kv* kv, const void* q, const void* k_new, const void* v_new,
                      const int32_t* positions, const tw_decode_params* prm, const tw_decode_buffers* buf,
                      cudaStream_t stream) {
+  // one CTA per unit streams its metadata and selects (unit.cu) when it covers the geometry
+  if (int s = tw_unit_select(kv, q, k_new, v_new, positions, prm, buf, stream); s != TW_FUSE_UNAVAILABLE) return s;
   if (!kv || !prm || !buf || !k_new || !v_new || !positions || kv->dtype != TW_BF16 ||
       prm->selector != TW_SELECT_QUEST || kv->head_dim != kHeadDim || kv->num_kv_heads < 1 ||
       kv->num_kv_heads > 32 || kv->num_seqs < 1 || kv->max_pages < 1 ||
@@ -400,6 +437,8 @@ extern "C" int tw_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
   if (prm->selector == TW_SELECT_QUEST &&
       (prm->budget_pages < 1 || !buf->page_scores || !buf->band_idx || !buf->band_scores || !q))
     return TW_ERR_INVALID;
+  if (prm->selector == TW_SELECT_QUEST)
+    if (int s = tw_unit_select(kv, q, nullptr, nullptr, nullptr, prm, buf, stream); s != TW_FUSE_UNAVAILABLE) return s;
   return kv->dtype == TW_BF16 ? launch_select<__nv_bfloat16>(kv, q, prm, buf, stream)
                               : launch_select<float>(kv, q, prm, buf, stream);
 }

@@ -433,7 +433,9 @@ static int launch_unit(const tw_paged_kv* kv, const tw_decode_params* prm, const
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int units = kv->num_seqs * kv->num_kv_heads;
-  if (G >= 2 && units * G <= sms && buf->topp_done) {  // few (unit, head) pairs: one CTA per query head
+  static const int force_head = getenv("TW_TOPP_HEAD") ? atoi(getenv("TW_TOPP_HEAD")) : -1;  // A/B knob
+  if (G >= 2 && buf->topp_done && (force_head > 0 || (force_head < 0 && units * G <= sms))) {
+    // few (unit, head) pairs: one CTA per query head
     const size_t smem = (size_t)kBins * 8 + (size_t)kHeadMC * 8;
     if (cudaFuncSetAttribute(topp_head_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)

@@ -295,7 +295,9 @@ __device__ __forceinline__ void unit_estimate(const int unit, const int b, const
 }
 
 // ---------------------------------------------------------------- the fused kernel
-template <int G, bool SB>
+// SELECT_ONLY: phases A + B only (K1 + K2: the candidate pages), for the
+// separate estimate / top-p kernels.
+template <int G, bool SB, bool SELECT_ONLY = false>
 __global__ void __launch_bounds__(kUnitThreads, 1) unit_step_kernel(tw_paged_kv kv, const __nv_bfloat16* __restrict__ q,
                                                                     tw_decode_params prm, tw_decode_buffers buf,
                                                                     const __nv_bfloat16* __restrict__ k_new,
@@ -341,6 +343,7 @@ __global__ void __launch_bounds__(kUnitThreads, 1) unit_step_kernel(tw_paged_kv 
   __syncthreads();
   UT(1);
   select_unit_body<__nv_bfloat16, kUnitThreads>(unit, kv, q, prm, buf, usm, n);
+  if constexpr (SELECT_ONLY) return;
   __syncthreads();
   UT(2);
   if (threadIdx.x == 0) s_ncand = buf.cand_count[unit];
@@ -352,6 +355,10 @@ __global__ void __launch_bounds__(kUnitThreads, 1) unit_step_kernel(tw_paged_kv 
   __syncthreads();
   topp_unit_body<G, UnitHB<G>::value, SB, UnitGT<G>::value>(unit, kv, prm, buf, usm);
   UT(4);
+}
+
+inline size_t unit_select_smem_bytes(int max_pages) {
+  return std::max<size_t>(kUfRing * kUnitWarps + 16 * 32 * sizeof(uint2), select_smem_bytes(max_pages, kUnitThreads));
 }
 
 template <int G>
@@ -433,6 +440,40 @@ static int launch_unit_step_g(const tw_paged_kv* kv, const void* q, const void* 
   if (words <= UnitCfg<G, UnitHB<G>::value, UnitGT<G>::value>::kBitsCap)
     return launch_unit_step<G, true>(kv, q, k_new, v_new, positions, prm, buf, stream);
   return launch_unit_step<G, false>(kv, q, k_new, v_new, positions, prm, buf, stream);
+}
+
+// K1 (when positions is given) + K2 in one per-unit launch: the Quest filter
+// streamed by the unit's CTA and its page selection (phases A + B above), for
+// the separate estimate and top-p kernels.  Returns TW_FUSE_UNAVAILABLE when
+// the geometry is not covered (nothing launched).
+int tw_unit_select(const tw_paged_kv* kv, const void* q, const void* k_new, const void* v_new,
+                   const int32_t* positions, const tw_decode_params* prm, const tw_decode_buffers* buf,
+                   cudaStream_t stream) {
+  const char* e = getenv("TW_USELECT");  // opt-in: measured no faster than quest_filter + quest_select (r02)
+  if (!e || atoi(e) == 0) return TW_FUSE_UNAVAILABLE;
+  if (!kv || !prm || !buf || !q || kv->dtype != TW_BF16 || kv->head_dim != kHeadDim ||
+      (kv->bits != 0 && kv->bits != 4) || prm->selector != TW_SELECT_QUEST || prm->budget_pages < 1 ||
+      !buf->page_scores || !buf->band_idx || !buf->band_scores || !buf->cand_pages || !buf->cand_count ||
+      !buf->counters || !buf->head_max || (positions && (!k_new || !v_new || positions == kv->seq_lens)))
+    return TW_FUSE_UNAVAILABLE;
+  const int G = kv->group_size;
+  if (G != 1 && G != 2 && G != 4) return TW_FUSE_UNAVAILABLE;
+  const size_t smem = unit_select_smem_bytes(kv->max_pages);
+  if (smem + 4096 > 227 * 1024) return TW_FUSE_UNAVAILABLE;
+  auto go = [&](auto kern) -> int {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return TW_ERR_CUDA;
+    cudaMemsetAsync(buf->counters, 0, 8 * sizeof(uint32_t), stream);
+    kern<<<kv->num_seqs * kv->num_kv_heads, kUnitThreads, smem, stream>>>(
+        *kv, (const __nv_bfloat16*)q, *prm, *buf, (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new,
+        positions);
+    return launch_status();
+  };
+  switch (G) {
+    case 1: return go(unit_step_kernel<1, false, true>);
+    case 2: return go(unit_step_kernel<2, false, true>);
+    default: return go(unit_step_kernel<4, false, true>);
+  }
 }
 
 // K1 (when positions is given) + K2 + K3 of one decode step in one launch.

@@ -1,15 +1,27 @@
 #!/bin/bash
 # One profiling pass for profiles/ (run on the GPU box):  tools/profile_round.sh <tag>
-#   bench lines (ours, reference arm, other configs), the launch list of the bench
-#   command (ncu gpu__time_duration, cold/serialised), one ncu --set full capture of
-#   the step's kernels (summary + per-stage DRAM traffic), GPU tests.
+#   GPU tests; bench lines C1-C5 (ours) and the reference arm; the launch list of
+#   the C2 bench command (ncu gpu__time_duration, cold/serialised); one ncu
+#   --set full capture of each config's step kernels (summary + per-stage DRAM
+#   traffic -> ncu_traffic.json); the opt-in fused per-unit kernel (TW_UNIT=1)
+#   bench line and phase trace (needs tools/_variants/utrace, built with
+#   tools/build_variant.sh utrace -DTW_UNIT_TRACE -DTW_TOPP_TRACE).
 set -u
 TAG=${1:-r01}
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 900 python bench.py > gpurun_out/bench_${TAG}_C2.json 2> gpurun_out/bench_${TAG}_C2.err; tail -c 400 gpurun_out/bench_${TAG}_C2.json
-timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_${TAG}_C2.json 2>&1; tail -c 300 gpurun_out/bench_ref_${TAG}_C2.json
-for c in C1 C3 C5; do timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_${TAG}_$c.json 2> gpurun_out/bench_${TAG}_$c.err; done
+python -m pytest tests -m gpu -x -q > gpurun_out/gputest_${TAG}.log 2>&1; tail -2 gpurun_out/gputest_${TAG}.log
+for c in C2 C1 C3 C5 C4; do
+  timeout 900 python bench.py --config $c $([ $c != C2 ] && echo --no-cpu-baseline) > gpurun_out/bench_${TAG}_$c.json 2> gpurun_out/bench_${TAG}_$c.err
+  tail -c 300 gpurun_out/bench_${TAG}_$c.json
+done
+for c in C2 C1 C3 C5; do
+  timeout 900 python bench.py --impl reference --config $c > gpurun_out/bench_ref_${TAG}_$c.json 2>&1
+done
+TW_UNIT=1 timeout 900 python bench.py --config C2 --no-cpu-baseline > gpurun_out/bench_${TAG}_C2_unit.json 2>&1
+for c in C2 C5 C3; do
+  TW_UNIT=1 TW_LIB_PATH=tools/_variants/utrace/libtwilight.so timeout 300 python tools/unit_trace.py --config $c \
+    --json gpurun_out/unit_trace_${TAG}_$c.json > /dev/null 2>&1
+done
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches_${TAG}_C2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 python tools/launches.py gpurun_out/launches_${TAG}_C2.csv --json gpurun_out/launches_${TAG}_C2.json | grep "tw::" || true
