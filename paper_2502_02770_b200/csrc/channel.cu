@@ -19,19 +19,20 @@
 // (rounding is monotone, so only the fp32 tie class of the k-th key is
 // ambiguous) and that class is ranked exactly by (fp64 score desc, token asc).
 // The union becomes the candidate pages plus a token mask the INT estimate
-// applies (tw_decode_buffers.tok_mask).  Contexts up to 32768 tokens per unit
-// (the keys of one head live in shared memory).
+// applies (tw_decode_buffers.tok_mask).  The ordered keys of the head being
+// selected live in the unit's logits rows (global memory, L2-resident: the
+// estimate overwrites them afterwards), so any context length is covered;
+// shared memory holds the histogram, the token bitmap and the tie band.
 #include "block_scan.cuh"
 
 namespace tw {
 
 constexpr int kChanThreads = 512;
-constexpr int kChanMaxTokens = 32768;
 constexpr int kChanBand = 4096;
 
 // byte offset of the fp64 band scores in dynamic shared memory (8-byte aligned)
 __host__ __device__ inline size_t chan_band_s_offset(int T_max) {
-  const size_t bytes = ((size_t)T_max + 2048 + (T_max + 31) / 32 + kChanBand) * 4;
+  const size_t bytes = ((size_t)2048 + (T_max + 31) / 32 + kChanBand) * 4;
   return (bytes + 7) & ~size_t(7);
 }
 
@@ -42,8 +43,7 @@ __global__ void __launch_bounds__(kChanThreads) chan_select_kernel(tw_paged_kv k
   extern __shared__ __align__(16) unsigned char smem[];
   const int T_max = kv.max_pages * kPage;
   const int words = (T_max + 31) / 32;
-  uint32_t* keys = reinterpret_cast<uint32_t*>(smem);          // [T_max]
-  uint32_t* hist = keys + T_max;                                 // [2048]
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);          // [2048]
   uint32_t* ubits = hist + 2048;                                 // [words]
   int* band_idx = reinterpret_cast<int*>(ubits + words);         // [kChanBand]
   double* band_s = reinterpret_cast<double*>(smem + chan_band_s_offset(T_max));  // [kChanBand]
@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(kChanThreads) chan_select_kernel(tw_paged_kv k
   __syncthreads();
   // ---- per head: top-B0 tokens, ties in the fp32 class of the k-th key ranked exactly
   for (int g = 0; g < (b0 > 0 ? G : 0); ++g) {
+    // the head's fp32 scores become ordered keys in place (its logits row, global memory)
+    uint32_t* keys = reinterpret_cast<uint32_t*>(zs + (size_t)g * Ts);
     for (int t = tid; t < n; t += kChanThreads) keys[t] = f2key(__ldcg(zs + (size_t)g * Ts + t));
     if (tid == 0) { s_namb = 0; s_cgt = 0; }
     __syncthreads();
@@ -191,10 +193,9 @@ int tw_select_channel_pruned(const tw_paged_kv* kv, const void* q, const tw_deco
   if (!kv || !q || !prm || !buf || kv->head_dim != kHeadDim || !buf->cand_pages || !buf->cand_count ||
       !buf->logits || !buf->tok_mask || !buf->chan_ids || !buf->head_max || !buf->counters || prm->budget_tokens < 1)
     return TW_ERR_INVALID;
-  if ((long long)kv->max_pages * kPage > kChanMaxTokens || kv->group_size > 8 || prm->top_channels < 0 ||
-      prm->top_channels > kHeadDim)
-    return TW_ERR_INVALID;
+  if (kv->group_size > 8 || prm->top_channels < 0 || prm->top_channels > kHeadDim) return TW_ERR_INVALID;
   const size_t smem = chan_smem_bytes(kv->max_pages);
+  if (smem > 200 * 1024) return TW_ERR_INVALID;  // token bitmap: contexts up to ~1.5 M tokens
   cudaMemsetAsync(buf->counters, 0, 8 * sizeof(uint32_t), stream);
   const int units = kv->num_seqs * kv->num_kv_heads;
   if (kv->dtype == TW_BF16) {

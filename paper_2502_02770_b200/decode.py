@@ -263,7 +263,7 @@ class TwilightDecoder:
     "sink_window" (the first ``sink`` + last ``window`` tokens, selectors.py:164-175), or
     "channel_pruned" (per query head the ``budget`` tokens with the largest
     partial logit over the ``top_channels`` channels of largest mean |K|,
-    selectors.py:135-161; contexts up to 32768 tokens).  ``estimator`` "int"
+    selectors.py:135-161; any context length).  ``estimator`` "int"
     estimates the candidates' logits from the cache's INT codes
     (quantcache.py:238-272), "exact" from the full-precision keys
     (estimator_bits="exact", pipeline.py:212-214).  With

@@ -72,7 +72,7 @@ def test_invalid_arguments_are_rejected_without_a_gpu():
     fake = ctypes.c_void_p(256)
     for name in ("cand_pages", "cand_count", "logits", "tok_mask", "chan_ids", "head_max", "counters"):
         setattr(buf, name, fake)
-    kv.max_pages = 4096  # 65536 tokens: beyond the selector's 32768-token shared-memory key array
+    kv.max_pages = 120000  # 1.92 M tokens: the token bitmap + tie band exceed the selector's shared memory
     assert lib.tw_select(ctypes.byref(kv), fake, ctypes.byref(prm), ctypes.byref(buf), None) == _lib.TW_ERR_INVALID
     kv.max_pages, prm.top_channels = 4, 129
     assert lib.tw_select(ctypes.byref(kv), fake, ctypes.byref(prm), ctypes.byref(buf), None) == _lib.TW_ERR_INVALID

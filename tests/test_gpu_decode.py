@@ -414,6 +414,32 @@ def test_channel_pruned_selector_batched(dtype, top_channels, budget):
                 np.testing.assert_allclose(to_np(out[b, h * G + g]), want, rtol=1e-4, atol=1e-4 * np.abs(want).max())
 
 
+def test_channel_pruned_selector_long_context():
+    """The channel-pruned selector beyond 32k tokens (keys staged in the unit's
+    logits rows, not shared memory): slice, per-head token sets and union at a
+    131,072-token context (selectors.py:135-161; the reference has no length cap)."""
+    B, H, G, n, budget, count = 1, 2, 4, 131072, 8192, 16
+    cache, batch = _cache(B, H, G, n, torch.bfloat16, [n], seed=41, tau=tau_schedule(H, (0.4, 1.5)))
+    dec = TwilightDecoder(cache, "channel_pruned", budget=budget, p=0.9)
+    q = batch.q.contiguous()
+    dec.select(q)
+    torch.cuda.synchronize()
+    bufs = dec.bufs
+    for h in range(H):
+        K = to_np(cache.unit_keys(0, h))
+        Qn = to_np(q[0, h * G:(h + 1) * G])
+        ids = orc.top_channels_by_magnitude(K, count)
+        np.testing.assert_array_equal(bufs.chan_ids[h, :count].cpu().numpy(), ids)
+        heads = [orc.channel_pruned_tokens(Qn[g], K, ids, budget) for g in range(G)]
+        want = orc.union_sorted(heads)
+        words = bufs.tok_mask[h].cpu().numpy().view(np.uint32)
+        got = np.flatnonzero(np.unpackbits(words.view(np.uint8), bitorder="little"))
+        if not np.array_equal(got, want):
+            assert all(_near_tie_ok(got, want, Qn[g], K, ids, budget) for g in range(G))
+        ncand = int(bufs.cand_count[h])
+        np.testing.assert_array_equal(bufs.cand_pages[h, :ncand].cpu().numpy(), np.unique(got // 16))
+
+
 def test_channel_pruned_fixed_slice_survives_appends():
     """fix_channels keeps the slice ranked at the first step (build_selector
     binds it once per context, selectors.py:203); without it every step

@@ -28,8 +28,9 @@ python tools/launches.py gpurun_out/launches_${TAG}_C2.csv --json gpurun_out/lau
 for c in C1 C2 C3 C5; do
   timeout 900 ncu --set full --import-source on --clock-control none \
     -k regex:"attn_kernel|quest_select|topp_unit|topp_head|estimate_kernel|quest_filter|append_kernel|merge_kernel|unit_step" -c 8 \
-    -o gpurun_out/full_${TAG}_$c python tools/prof_step.py --config $c --reps 1 > /dev/null 2>&1
-  python tools/ncu_hot.py gpurun_out/full_${TAG}_$c.ncu-rep . --lines 6 > gpurun_out/ncu_full_${TAG}_$c.txt 2>&1
-  python tools/traffic_json.py gpurun_out/full_${TAG}_$c.ncu-rep $c > gpurun_out/traffic_${TAG}_$c.json 2>&1 || true
+    -o /tmp/full_${TAG}_$c python tools/prof_step.py --config $c --reps 1 > /dev/null 2>&1
+  # reports stay on the box (gpurun_out/ merges back only up to 64 MiB): summaries + traffic come back
+  python tools/ncu_hot.py /tmp/full_${TAG}_$c.ncu-rep . --lines 6 > gpurun_out/ncu_full_${TAG}_$c.txt 2>&1
+  python tools/traffic_json.py /tmp/full_${TAG}_$c.ncu-rep $c > gpurun_out/traffic_${TAG}_$c.json 2>&1 || true
 done
 cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json
