@@ -953,12 +953,17 @@ def main():
     ap.add_argument("--waves", type=int, default=1, help="sub-batches pipelined on separate streams (1 = off; measured slower at C2)")
     ap.add_argument("--cpu-units", type=int, default=8)
     ap.add_argument("--chunk", type=int, default=0, help="attention work-item tokens (0: auto)")
+    ap.add_argument("--ctx", type=int, default=0, help="context length override (budget scaled with it)")
     ap.add_argument("--p", default="", help="comma-separated top-p sweep (default: the config's own, C5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = dict(CONFIGS[args.config])
+    if args.ctx:  # context override (e.g. the C1 batch-1 sparse/dense crossover); budget scales as n/4
+        scale = args.ctx / cfg["n"]
+        cfg.update(n=args.ctx, budget=int(cfg["budget"] * scale) if cfg["budget"] else None,
+                   desc=cfg["desc"] + f" [ctx override {args.ctx}]")
     if args.impl == "reference":
         run_reference(args, cfg)
     elif cfg.get("model"):
