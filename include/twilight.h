@@ -226,6 +226,21 @@ int tw_topp_bisect(const double* weights, int32_t rows, int32_t n, double p, dou
                    int32_t max_iters, uint8_t* mask_out, double* threshold_out,
                    int32_t* iters_out, cudaStream_t stream);
 
+/* Per-vector operators of the reference API (off the decode path):
+ *   tw_vec_logits  out[n] f32 = K[n][d] q[d] / float32(sqrt d)      attention.py:102 (attention_weights)
+ *   tw_vec_softmax out[n] f32 = exp(z - max z) / sum, scratch >= 16 B attention.py:79-86 (stable_softmax)
+ *   tw_vec_readout out[d] = w[idx] @ V[idx] (/ sum w[idx] if renorm), weights f32 (TW_F32) or f64 (2),
+ *                  values f32 / bf16; out in the weights' type; partial: tw_vec_readout_parts() * (d+1)
+ *                  doubles of scratch; *mass_out = sum w[idx]       attention.py:106-136 (sparse_attention)
+ * dtype / vdtype are tw_dtype codes. */
+int tw_vec_logits(const void* q, const void* keys, int64_t n, int32_t d, int32_t dtype, float* out,
+                  cudaStream_t stream);
+int tw_vec_softmax(const float* z, int64_t n, float* out, void* scratch, cudaStream_t stream);
+int32_t tw_vec_readout_parts(void);
+int tw_vec_readout(const void* w, int32_t wdtype, const void* v, int32_t vdtype, int64_t n, int32_t d,
+                   const int64_t* idx, int64_t m, int32_t renorm, void* out, double* partial, double* mass_out,
+                   cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,7 +36,8 @@ EXPORTS = (
     "tw_version", "tw_max_work_items", "tw_quant_append", "tw_quant_build", "tw_quant_rows",
     "tw_quest_scores", "tw_select", "tw_estimate", "tw_topp", "tw_sparse_attention",
     "tw_dense_attention", "tw_decode_step", "tw_estimate_tokens", "tw_topp_bisect", "tw_select_estimate_topp",
-    "tw_select_estimate_topp_applies",
+    "tw_select_estimate_topp_applies", "tw_vec_logits", "tw_vec_softmax", "tw_vec_readout_parts",
+    "tw_vec_readout",
 )
 
 
@@ -109,6 +110,10 @@ def lib() -> ctypes.CDLL:
         "tw_topp_bisect": ([P, I32, I32, ctypes.c_double, ctypes.c_double, I32, P, P, P, P], ctypes.c_int),
         "tw_select_estimate_topp": ([P, P, P, P, P, P, P, P], ctypes.c_int),
         "tw_select_estimate_topp_applies": ([P, P, P], I32),
+        "tw_vec_logits": ([P, P, ctypes.c_int64, I32, I32, P, P], ctypes.c_int),
+        "tw_vec_softmax": ([P, ctypes.c_int64, P, P, P], ctypes.c_int),
+        "tw_vec_readout_parts": ([], I32),
+        "tw_vec_readout": ([P, I32, P, I32, ctypes.c_int64, I32, P, ctypes.c_int64, I32, P, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

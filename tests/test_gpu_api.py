@@ -436,3 +436,33 @@ def test_prebuilt_cache_is_reused(monkeypatch):
 def replace_bits(cfg, bits):
     from dataclasses import replace
     return replace(cfg, estimator_bits=bits)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("n,d", [(1, 128), (1000, 128), (131072, 128), (777, 64)])
+def test_vector_operators_match_fp32_reference(dtype, n, d):
+    """attention_weights / stable_softmax / sparse_attention on the tw_vec_*
+    kernels vs a plain fp32 (fp64 for the readout) torch reference of the same
+    op (attention.py:79-136)."""
+    g = torch.Generator(device="cuda").manual_seed(n + d)
+    K = torch.randn(n, d, device="cuda", generator=g).to(dtype)
+    V = torch.randn(n, d, device="cuda", generator=g).to(dtype)
+    q = (torch.randn(d, device="cuda", generator=g) * 2).to(dtype)
+    w = tw.attention_weights(q, K)
+    assert w.dtype == dtype
+    z = (K.float() @ q.float()) / np.float32(np.sqrt(d))
+    ref = torch.softmax(z.double(), 0)
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    torch.testing.assert_close(w.double(), ref, rtol=tol, atol=tol * float(ref.max()))
+    s = tw.stable_softmax(z)
+    torch.testing.assert_close(s.double(), ref, rtol=1e-5, atol=1e-7 * float(ref.max()) + 1e-12)
+    idx = torch.unique(torch.randint(0, n, (max(1, n // 3),), device="cuda", generator=g))
+    sel = tw.TokenSelection.from_indices(idx, n)
+    for wts in (w.float(), ref):  # fp32 and fp64 weights
+        for renorm in (False, True):
+            got = tw.sparse_attention(wts, V, sel, renormalize=renorm)
+            want = wts.double()[idx] @ V.double()[idx]
+            if renorm:
+                want = want / wts.double()[idx].sum()
+            assert got.dtype == torch.promote_types(wts.dtype, V.dtype)
+            torch.testing.assert_close(got.double(), want, rtol=1e-5, atol=1e-6 * float(want.abs().max()) + 1e-12)
