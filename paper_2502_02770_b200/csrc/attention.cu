@@ -34,7 +34,7 @@ constexpr int kTile = 16;               // rows per stage
 constexpr int kNS = TW_ATT_STAGES;      // stages per warp
 constexpr int kMaxChunk = 512;          // tokens per work item (upper bound)
 constexpr int kDefaultChunk = TW_DEFAULT_CHUNK;
-constexpr int kDenseChunk = 512;
+constexpr int kDenseChunk = 512;  // dense work-item tokens once the batch fills the GPU (see dense_chunk)
 
 template <typename T>
 struct WarpSmem {
@@ -438,18 +438,25 @@ __global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const
 
 // Merge the split-KV partials of every unit with more than one item
 // (log-sum-exp over the union of the items, attention.py:130-135): one CTA of
-// 128 threads per (unit, head).  Thread i < n loads item i's (m, l) -- one
-// round of loads for every item -- the CTA reduces the max and the weights,
-// then thread c sums item outputs o_ic with all loads of a batch in flight.
+// kMergeThreads per (unit, head).  Every thread loads item maxima / masses
+// (one round of loads for up to kMergeThreads items), the CTA reduces the max
+// and the weights, then kMergeGroups groups of 128 threads each sum a quarter
+// of the items' outputs for channel (tid % 128) with their loads in flight,
+// and the groups' sums are added in a fixed order.
+constexpr int kMergeGroups = 4;
+constexpr int kMergeThreads = kMergeGroups * kHeadDim;
+
 template <int G, bool DENSE>
-__global__ void __launch_bounds__(kHeadDim) merge_kernel(tw_paged_kv kv, tw_decode_buffers buf, float* __restrict__ out,
-                                                         int chunk, int max_chunks) {
+__global__ void __launch_bounds__(kMergeThreads) merge_kernel(tw_paged_kv kv, tw_decode_buffers buf,
+                                                              float* __restrict__ out, int chunk, int max_chunks) {
   pdl_wait();
   pdl_trigger();
   constexpr int kMaxItems = 1024;
+  constexpr int NW = kMergeThreads / 32;
   __shared__ float e_s[kMaxItems];
-  __shared__ float red[kHeadDim / 32], red2[kHeadDim / 32];
-  const int unit = blockIdx.x / G, g = blockIdx.x % G, c = threadIdx.x, lane = c & 31, warp = c >> 5;
+  __shared__ float red[NW], red2[NW];
+  __shared__ float osum[kMergeGroups][kHeadDim];
+  const int unit = blockIdx.x / G, g = blockIdx.x % G, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int first, n;
   if (DENSE) {
     const int len = kv.seq_lens[unit / kv.num_kv_heads];
@@ -464,7 +471,7 @@ __global__ void __launch_bounds__(kHeadDim) merge_kernel(tw_paged_kv kv, tw_deco
   const float* P = buf.partials + (size_t)first * kStride + g * (kHeadDim + 2);
   // item maxima (n <= kMaxItems: tw_max_work_items bounds the items of one unit)
   float mloc = -INFINITY;
-  for (int i = c; i < n; i += kHeadDim) {
+  for (int i = tid; i < n; i += kMergeThreads) {
     const float mi = P[(size_t)i * kStride + kHeadDim];
     e_s[i] = mi;
     mloc = fmaxf(mloc, mi);
@@ -474,9 +481,9 @@ __global__ void __launch_bounds__(kHeadDim) merge_kernel(tw_paged_kv kv, tw_deco
   __syncthreads();
   float M = red[0];
 #pragma unroll
-  for (int w = 1; w < kHeadDim / 32; ++w) M = fmaxf(M, red[w]);
+  for (int w = 1; w < NW; ++w) M = fmaxf(M, red[w]);
   float lloc = 0.f;
-  for (int i = c; i < n; i += kHeadDim) {
+  for (int i = tid; i < n; i += kMergeThreads) {
     const float mi = e_s[i];
     const float e = mi == -INFINITY ? 0.f : __expf(mi - M);
     e_s[i] = e;
@@ -487,18 +494,26 @@ __global__ void __launch_bounds__(kHeadDim) merge_kernel(tw_paged_kv kv, tw_deco
   __syncthreads();
   float L = 0.f;
 #pragma unroll
-  for (int w = 0; w < kHeadDim / 32; ++w) L += red2[w];
+  for (int w = 0; w < NW; ++w) L += red2[w];
+  const int grp = tid / kHeadDim, c = tid % kHeadDim;
   float O = 0.f;
-  int i = 0;
-  for (; i + 16 <= n; i += 16) {
-    float o[16];
+  int i = grp;
+  for (; i + 8 * kMergeGroups <= n; i += 8 * kMergeGroups) {
+    float o[8];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) o[k] = P[(size_t)(i + k) * kStride + c];
+    for (int k = 0; k < 8; ++k) o[k] = P[(size_t)(i + k * kMergeGroups) * kStride + c];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) O = fmaf(e_s[i + k], o[k], O);
+    for (int k = 0; k < 8; ++k) O = fmaf(e_s[i + k * kMergeGroups], o[k], O);
   }
-  for (; i < n; ++i) O = fmaf(e_s[i], P[(size_t)i * kStride + c], O);
-  out[((size_t)unit * G + g) * kHeadDim + c] = L > 0.f ? O / L : 0.f;
+  for (; i < n; i += kMergeGroups) O = fmaf(e_s[i], P[(size_t)i * kStride + c], O);
+  osum[grp][c] = O;
+  __syncthreads();
+  if (grp == 0) {
+    float t = osum[0][c];
+#pragma unroll
+    for (int k = 1; k < kMergeGroups; ++k) t += osum[k][c];
+    out[((size_t)unit * G + g) * kHeadDim + c] = L > 0.f ? t / L : 0.f;
+  }
 }
 
 }  // namespace tw
@@ -537,7 +552,7 @@ static int launch_attn(const tw_paged_kv* kv, const T* q, const tw_decode_buffer
   if (DENSE && grid * kAttWarps > total) grid = (total + kAttWarps - 1) / kAttWarps;
   if (DENSE) cudaMemsetAsync(buf->counters + 5, 0, sizeof(uint32_t), s);  // dense runs without tw_select
   launch_pdl(kern, dim3(grid), dim3(kAttThreads), smem, s, *kv, q, *buf, out, chunk, max_chunks, total);
-  launch_pdl(merge_kernel<G, DENSE>, dim3(units * G), dim3(kHeadDim), 0, s, *kv, *buf, out, chunk, max_chunks);
+  launch_pdl(merge_kernel<G, DENSE>, dim3(units * G), dim3(kMergeThreads), 0, s, *kv, *buf, out, chunk, max_chunks);
   return launch_status();
 }
 
@@ -566,14 +581,34 @@ extern "C" int tw_sparse_attention(const tw_paged_kv* kv, const void* q, const t
   TW_DISPATCH_G(kv->group_size, (launch_attn<float, GG, false>(kv, (const float*)q, buf, out, chunk, stream)))
 }
 
+// Dense work-item size: 512 tokens once units x chunks give every worker warp
+// of a full GPU (148 SMs x 12 warps) two items; smaller (down to 64, multiples
+// of 16) for small batches, which would otherwise leave most SMs idle (batch 1
+// x 8 KV heads at 8k: 136 items of 512 for 1776 workers); never more than 1024
+// items per unit (the merge kernel's bound).
+static int dense_chunk(const tw_paged_kv* kv) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t units = (int64_t)kv->num_seqs * kv->num_kv_heads;
+  const int64_t T = (int64_t)kv->max_pages * kPage;
+  const int64_t target = (int64_t)sms * 3 * kAttWarps * 2;
+  int64_t c = (T * units + target - 1) / target;
+  c = (c + kTile - 1) / kTile * kTile;
+  c = c < 64 ? 64 : c > kDenseChunk ? kDenseChunk : c;
+  const int64_t floor1024 = ((T + 1023) / 1024 + kTile - 1) / kTile * kTile;
+  return (int)(c < floor1024 ? floor1024 : c);
+}
+
 extern "C" int tw_dense_attention(const tw_paged_kv* kv, const void* q, const tw_decode_buffers* buf, float* out,
                                   cudaStream_t stream) {
   if (!kv || !q || !buf || !out || kv->head_dim != kHeadDim || !buf->partials) return TW_ERR_INVALID;
+  const int chunk = dense_chunk(kv);
   if (kv->dtype == TW_BF16) {
     TW_DISPATCH_G(kv->group_size,
-                  (launch_attn<__nv_bfloat16, GG, true>(kv, (const __nv_bfloat16*)q, buf, out, kDenseChunk, stream)))
+                  (launch_attn<__nv_bfloat16, GG, true>(kv, (const __nv_bfloat16*)q, buf, out, chunk, stream)))
   }
-  TW_DISPATCH_G(kv->group_size, (launch_attn<float, GG, true>(kv, (const float*)q, buf, out, kDenseChunk, stream)))
+  TW_DISPATCH_G(kv->group_size, (launch_attn<float, GG, true>(kv, (const float*)q, buf, out, chunk, stream)))
 }
 
 extern "C" int64_t tw_max_work_items(const tw_paged_kv* kv, int32_t chunk_tokens) {
@@ -582,6 +617,7 @@ extern "C" int64_t tw_max_work_items(const tw_paged_kv* kv, int32_t chunk_tokens
   const int64_t T = (int64_t)kv->max_pages * kPage;
   const int64_t c = chunk_tokens > 0 ? chunk_tokens : kDefaultChunk;
   const int64_t sparse = units * ((T + c - 1) / c);
-  const int64_t dense = units * ((T + kDenseChunk - 1) / kDenseChunk);
+  const int64_t dc = dense_chunk(kv);
+  const int64_t dense = units * ((T + dc - 1) / dc);
   return sparse > dense ? sparse : dense;
 }
