@@ -280,22 +280,46 @@ __global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const
     const ItemDesc d = get_item<DENSE>(kv, buf, it, chunk, max_chunks);
     if (d.count <= 0) continue;
     const int b = d.unit / H, h = d.unit % H;
-    // row indices of the whole item (all index loads in flight together)
-    {
-      const int* pt = kv.page_table + (size_t)b * kv.max_pages;
-      const int* ids = DENSE ? nullptr : buf.final_idx + d.unit * T_stride + d.start;
-      __syncwarp();
-      for (int j = lane; j < d.count; j += 32) {
-        const int tok = DENSE ? d.start + j : __ldg(ids + j);
-        W.rows[j] = ((uint32_t)__ldg(pt + (tok >> 4)) * H + h) * kPage + (tok & 15);
-      }
-      __syncwarp();
-    }
+    // Row indices (token id -> page table -> row): the first 32 rows (the
+    // ring's first stages) are resolved first and their copies issued, then
+    // the rest resolve while those copies are in flight, all loads of a batch
+    // in flight together (two dependent L2 round trips per 8 rows otherwise
+    // stalled every item's start).
+    const int* pt = kv.page_table + (size_t)b * kv.max_pages;
+    const int* ids = DENSE ? nullptr : buf.final_idx + d.unit * T_stride + d.start;
+    auto row_of = [&](int j) -> uint32_t {
+      const int tok = DENSE ? d.start + j : __ldg(ids + j);
+      return ((uint32_t)__ldg(pt + (tok >> 4)) * H + h) * kPage + (tok & 15);
+    };
+    __syncwarp();
+    if (lane < d.count) W.rows[lane] = row_of(lane);
+    __syncwarp();
     const int nst = (d.count + kTile - 1) / kTile;
+    static_assert((kNS - 1) * kTile <= 32, "the prologue stages use the first 32 rows");
 #pragma unroll
     for (int s = 0; s < kNS - 1; ++s) {
       if (s < nst) issue_stage<T>(W, kv, s, d.count, s);
       cp_commit();
+    }
+    {
+      constexpr int kB = 8;  // rows per lane resolved together
+      for (int j0 = 32; j0 < d.count; j0 += 32 * kB) {
+        int tok[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int j = j0 + 32 * u + lane;
+          tok[u] = j < d.count ? (DENSE ? d.start + j : __ldg(ids + j)) : 0;
+        }
+        uint32_t ph[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) ph[u] = j0 + 32 * u + lane < d.count ? (uint32_t)__ldg(pt + (tok[u] >> 4)) : 0u;
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int j = j0 + 32 * u + lane;
+          if (j < d.count) W.rows[j] = (ph[u] * H + h) * kPage + (tok[u] & 15);
+        }
+      }
+      __syncwarp();
     }
     const T* qu = q + (size_t)d.unit * G * kHeadDim;
     float* part = buf.partials + (size_t)d.slot * G * (kHeadDim + 2);

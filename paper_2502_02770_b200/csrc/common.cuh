@@ -211,7 +211,7 @@ inline bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("TW_PDL");
-    on = e ? atoi(e) != 0 : 0;  // measured no gain inside CUDA graphs (r01): off by default
+    on = e ? atoi(e) != 0 : 1;  // r02: C1 61.4 -> 58.6 us, C2 e2e 319.6 -> 312.3 us, C2 step unchanged
   }
   return on != 0;
 }
