@@ -139,13 +139,12 @@ __device__ __forceinline__ void select_unit_body(const int unit, const tw_paged_
       const float* sc = buf.page_scores + qhi * Pmax;
       int* band_idx = buf.band_idx + qhi * Pmax;
       double* band_s = buf.band_scores + qhi * Pmax;
-      // margin: ||q||_1 * max|k| * 300 u  (+ relative slack so fp64-divide ties are rescored)
-      if (wig == 0) {
-        float qa = 0.f;
-        for (int c = lane; c < kHeadDim; c += 32) qa += fabsf(Elem<T>::to_f(qh[c]));
-        qa = warp_sum(qa);
-        if (lane == 0) { gs.margin = qa * amax * (300.0f / 16777216.0f); gs.namb = 0; gs.cin = 0; }
-      }
+      // margin: ||q||_1 * max|k| * 300 u  (+ relative slack so fp64-divide ties are rescored);
+      // its q loads are issued before, and summed after, the key loads
+      float qv[kHeadDim / 32];
+      if (wig == 0)
+#pragma unroll
+        for (int c = 0; c < kHeadDim / 32; ++c) qv[c] = fabsf(Elem<T>::to_f(qh[lane + 32 * c]));
       for (int i = grp.tid; i < words; i += grp.nthreads) hbits[i] = 0;
       if ((Pmax & 3) == 0) {  // rows 16-byte aligned: four scores per load, all in flight at once
         const int P4 = P >> 2;
@@ -162,21 +161,41 @@ __device__ __forceinline__ void select_unit_body(const int unit, const tw_paged_
 #pragma unroll 8
         for (int i = grp.tid; i < P; i += grp.nthreads) keys[i] = f2key(__ldcg(sc + i));
       }
+      if (wig == 0) {
+        float qa = 0.f;
+#pragma unroll
+        for (int c = 0; c < kHeadDim / 32; ++c) qa += qv[c];
+        qa = warp_sum(qa);
+        if (lane == 0) { gs.margin = qa * amax * (300.0f / 16777216.0f); gs.namb = 0; gs.cin = 0; }
+      }
       grp.sync();
       STRACE();
-      const float t = key2f(group_kth_largest_lin(grp, keys, P, (uint32_t)k, hist, gs.mem, gs.tmp, gs.res));
+      // the k-th largest fp32 bound, exactly (a bin-wide window instead made the band --
+      // rescored in fp64 -- wider and the select slower: C2 K2 51 -> 55 us, C5 250 -> 282 us)
+      const float tlo = key2f(group_kth_largest_lin(grp, keys, P, (uint32_t)k, hist, gs.mem, gs.tmp, gs.res));
+      const float thi = tlo;
       STRACE();
-      const float m2 = 2.f * gs.margin + 1e-6f * fabsf(t) + 1e-30f;
-      const float hi_cut = t + m2, lo_cut = t - m2;
-      for (int i = grp.tid; i < P; i += grp.nthreads) {
-        const float s = key2f(keys[i]);
-        if (s > hi_cut) {
-          atomicOr(&hbits[i >> 5], 1u << (i & 31));
-          atomicAdd(&gs.cin, 1);
-        } else if (s >= lo_cut) {
-          band_idx[atomicAdd(&gs.namb, 1)] = i;
+      const float m2 = 2.f * gs.margin + 1e-6f * fmaxf(fabsf(tlo), fabsf(thi)) + 1e-30f;
+      const float hi_cut = thi + m2, lo_cut = tlo - m2;
+      // classify 32 consecutive pages per warp: in-set bits by ballot, band members appended
+      // with one shared atomic per warp
+      uint32_t cin = 0;
+      for (int i0 = grp.tid - lane; i0 < P; i0 += grp.nthreads) {
+        const int i = i0 + lane;
+        const float sv = i < P ? key2f(keys[i]) : -INFINITY;
+        const bool in = i < P && sv > hi_cut;
+        const bool band = i < P && !in && sv >= lo_cut;
+        const uint32_t bin_ = __ballot_sync(0xffffffffu, in), bband = __ballot_sync(0xffffffffu, band);
+        if (lane == 0) hbits[i0 >> 5] = bin_;
+        cin += __popc(bin_);
+        if (bband) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&gs.namb, __popc(bband));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (band) band_idx[base + __popc(bband & ((1u << lane) - 1u))] = i;
         }
       }
+      if (lane == 0 && cin) atomicAdd(&gs.cin, (int)cin);
       grp.sync();
       STRACE();
       const int namb = gs.namb;
