@@ -183,7 +183,9 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
   int cur_unit = -1;
   for (int it = warp_fetch(ctr); it < units * max_chunks; it = warp_fetch(ctr)) {
     const int unit = it % units;
-    const int p0 = (it / units) * item;
+    // chunks in reverse order: the item holding the open page (the append, a
+    // latency chain) is taken first instead of last
+    const int p0 = (max_chunks - 1 - it / units) * item;
     const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
     const int pos = positions ? __ldg(positions + b) : -1;
     const int n = positions ? min(pos + 1, kv.max_pages * kPage) : kv.seq_lens[b];

@@ -74,6 +74,19 @@ static __device__ __noinline__ float bin_ceiling(int b, float M, float M120) {
   }
   return x;
 #endif
+  // fast path: the edge is usually within a few ulps of the guess
+  {
+    float x = e;
+    int i = 0;
+    for (; i < 8 && dbin(x, M120) < b; ++i) x = nextafterf(x, -INFINITY);
+    if (i < 8) {
+      for (i = 0; i < 8; ++i) {
+        const float up = nextafterf(x, INFINITY);
+        if (dbin(up, M120) < b) return x;
+        x = up;
+      }
+    }
+  }
   const float d = 2e-3f;  // a quarter bin
   uint32_t lo = f2key(e - d), hi = f2key(e + d);  // dbin(lo) >= b > dbin(hi)
   while (hi - lo > 1) {
@@ -621,6 +634,9 @@ __device__ __forceinline__ void topp_unit_body(const int unit, const tw_paged_kv
   __shared__ uint32_t s_wtot[NW];
   const int per_w = (words + NW - 1) / NW;
   const int wlo = min(words, warp * per_w), whi = min(words, wlo + per_w);
+  // the first emission group's candidate pages, loaded ahead of the count and the CTA scan
+  const int pa0 = 2 * wlo + lane < kv.max_pages ? __ldcg(cand + 2 * wlo + lane) : 0;
+  const int pb0 = 2 * wlo + 32 + lane < kv.max_pages ? __ldcg(cand + 2 * wlo + 32 + lane) : 0;
   uint32_t cnt = 0;
   for (int w = wlo + lane; w < whi; w += 32) cnt += __popc(ld_bits(w));
   cnt = warp_sum(cnt);
@@ -642,8 +658,8 @@ __device__ __forceinline__ void topp_unit_body(const int unit, const tw_paged_kv
   for (int w0 = wlo; w0 < whi; w0 += 32) {
     const int w = w0 + lane;
     const uint32_t x = w < whi ? ld_bits(w) : 0u;
-    const int pa = 2 * w0 + lane < kv.max_pages ? cand[2 * w0 + lane] : 0;
-    const int pb = 2 * w0 + 32 + lane < kv.max_pages ? cand[2 * w0 + 32 + lane] : 0;
+    const int pa = w0 == wlo ? pa0 : 2 * w0 + lane < kv.max_pages ? cand[2 * w0 + lane] : 0;
+    const int pb = w0 == wlo ? pb0 : 2 * w0 + 32 + lane < kv.max_pages ? cand[2 * w0 + 32 + lane] : 0;
     uint32_t incl = __popc(x);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
