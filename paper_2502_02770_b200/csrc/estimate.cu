@@ -36,10 +36,16 @@ namespace tw {
 constexpr int kEstPagesPerCta = TW_EST_ITEM;  // candidate pages per work item (<= 32: one per lane)
 constexpr int kEstWarps = 4;
 
-constexpr int kEstStages = TW_EST_STAGES;  // pages in flight per warp (cp.async ring)
+constexpr int kEstStages = TW_EST_STAGES;  // pages in flight per warp (ring stages)
+#ifndef TW_EST_BULK
+#define TW_EST_BULK 0  // r02: bulk copies measured 1-2% slower (C2 47.5 vs 46.9 us, C3 401 vs 392 us)
+#endif
 
 // Persistent warp workers over (unit, 32-candidate-page) items, chunk-major;
-// each warp streams its pages' 1152-B INT4 blocks through a 4-deep cp.async ring.
+// each warp streams its pages' 1152-B INT4 blocks through a 4-deep ring of
+// 72 16-byte cp.async per page; built with -DTW_EST_BULK=1 every page is ONE
+// TMA bulk copy (cp.async.bulk, issued by the lane that holds the page's
+// address) completing on a per-stage mbarrier (measured 1-2% slower).
 // MASKED: the sink-window or channel-pruned selectors' token masks are
 // applied; the plain (Quest / full) variant drops those per-page tests.
 template <typename T, int G, int BITS, bool MASKED>
@@ -54,6 +60,13 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
   constexpr int kBlock = qblock_bytes_for(BITS), kCodes = code_bytes_for(BITS), kRowBytes = kHeadDim * BITS / 8;
   __shared__ __align__(128) uint8_t ring[kEstWarps][kSt][kBlock];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#if TW_EST_BULK
+  __shared__ __align__(8) uint64_t bars[kEstWarps][kSt];
+  if (lane < kSt) mbar_init(&bars[warp][lane], 1);
+  mbar_fence_init();
+  __syncwarp();
+  uint32_t issued = 0;  // pages this warp has issued: page j of all items uses slot j % kSt, parity (j / kSt) & 1
+#endif
   const int t = lane & 3, r = lane >> 2;
   const int units = kv.num_seqs * kv.num_kv_heads;
   const int T_stride = kv.max_pages * kPage;
@@ -101,6 +114,18 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       lp_l = buf.cand_pages[(size_t)unit * kv.max_pages + c0 + lane];
       src_l = kv.kq + ((size_t)kv.page_table[(size_t)b * kv.max_pages + lp_l] * kv.num_kv_heads + h) * kBlock;
     }
+#if TW_EST_BULK
+    const uint32_t base = issued;
+    auto issue = [&](int i) {
+      const uint32_t slot = (base + i) % kSt;
+      if (lane == 0) mbar_arrive_expect_tx(&bars[warp][slot], kBlock);
+      __syncwarp();
+      if (lane == i) bulk_g2s(R[slot], src_l, kBlock, &bars[warp][slot]);
+    };
+#pragma unroll
+    for (int i = 0; i < kSt - 1; ++i)
+      if (i < np) issue(i);
+#else
     auto issue = [&](int i) {
       const uint8_t* src = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, (unsigned long long)src_l, i));
       uint8_t* dst = R[i % kSt];
@@ -112,6 +137,7 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
       if (i < np) issue(i);
       cp_commit();
     }
+#endif
     if (unit != cur_unit) {
       if (cur_unit >= 0) flush_max(cur_unit);
       if constexpr (kPacked) estimate_prologue_packed<T, G, BITS>(q, unit, pb1, pb2, sq[0], isc[0]);
@@ -120,10 +146,16 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
     }
     for (int i = 0; i < np; ++i) {
       if (i + kSt - 1 < np) issue(i + kSt - 1);
+#if TW_EST_BULK
+      const uint32_t slot = (base + i) % kSt;
+      mbar_wait(&bars[warp][slot], ((base + i) / kSt) & 1);
+      const uint8_t* pg = R[slot];
+#else
       cp_commit();
       cp_wait<kSt - 1>();
       __syncwarp();
       const uint8_t* pg = R[i % kSt];
+#endif
       // the lane's code bytes of rows r and r+8: channels 32t .. 32t+31
       uint32_t wl[BITS], wh[BITS];
       if (BITS == 8) {
@@ -232,7 +264,11 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
         }
       }
     }
+#if TW_EST_BULK
+    issued = base + np;  // every issued page was waited on above
+#else
     cp_wait<0>();
+#endif
   }
   if (cur_unit >= 0) flush_max(cur_unit);
 }
