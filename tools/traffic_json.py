@@ -14,7 +14,7 @@ STAGES = {
     "K1_append": ["append_kernel"],
     "K2_select": ["quest_filter", "quest_select"],
     "K3a_estimate": ["estimate_kernel"],
-    "K3bc_topp": ["topp_unit"],
+    "K3bc_topp": ["topp_unit", "topp_head"],
     "K4_attention": ["attn_kernel", "merge_kernel"],
     "K23_unit": ["unit_step"],
 }
