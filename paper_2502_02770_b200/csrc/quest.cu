@@ -135,17 +135,11 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_kernel(tw_paged_kv
 // (bf16 products exact, fp32 accumulation, covered by the select margin).
 // Per warp: 16-page tiles (16 x 512 B, XOR-swizzled rows) through a TW_QM_STAGES-deep (2)
 // cp.async ring; one ldmatrix.x4 + one MMA per page-tile k-step.
-// TW_QM_TILE = 8: 8-page tiles with the MMA roles swapped (the G query rows are
-// the A operand, the tile's pages the N = 8 columns), so the same 16 KB per
-// warp holds 4 stages -- 3 tiles (12 KB) in flight instead of one 8 KB tile.
-#ifndef TW_QM_TILE
-#define TW_QM_TILE 16
-#endif
 #ifndef TW_QM_STAGES
-#define TW_QM_STAGES (TW_QM_TILE == 8 ? 4 : 2)
+#define TW_QM_STAGES 2
 #endif
 constexpr int kQmStages = TW_QM_STAGES;
-constexpr int kQmTile = TW_QM_TILE;  // pages per stage: 16 (pages = MMA rows) or 8 (pages = MMA columns)
+constexpr int kQmTile = 16;  // pages per stage (= the MMA's rows)
 
 __device__ __forceinline__ void ldsm_x4_q(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -258,7 +252,7 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
       __syncwarp();
       const uint8_t* tile = R[s % kQmStages];
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      if constexpr (kQmTile == 16) {
+      {
         const int row = (q8 & 1) * 8 + rr;
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) {
@@ -275,168 +269,10 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
           const int g = 2 * t + (e & 1);
           if (g < G && pg < np) scores[((size_t)unit * G + g) * kv.max_pages + p0 + pg] = acc[e];
         }
-      } else {
-        // A = the q fragments (row r = head r, rows >= 8 zero: the same registers as the
-        // B fragments above), B = 8 page rows: ldmatrix matrix q8 = chunk 4kk2 + q8, row rr = page
-#pragma unroll
-        for (int kk2 = 0; kk2 < 8; ++kk2) {
-          uint32_t bf[4];
-          const int chunk = 4 * kk2 + q8;
-          ldsm_x4_q(bf, tile + rr * 512 + ((chunk ^ rr) << 4));
-          const uint32_t a0[4] = {qb[2 * kk2][0], 0u, qb[2 * kk2][1], 0u};
-          const uint32_t a1[4] = {qb[2 * kk2 + 1][0], 0u, qb[2 * kk2 + 1][1], 0u};
-          mma_bf16_q(acc, a0, bf[0], bf[1]);
-          mma_bf16_q(acc, a1, bf[2], bf[3]);
-        }
-        __syncwarp();
-        // row r (head), cols 2t, 2t+1 (pages)
-        if (r < G) {
-          const int pg = 8 * s + 2 * t;
-          float* so = scores + ((size_t)unit * G + r) * kv.max_pages + p0;
-          if (pg < np) so[pg] = acc[0];
-          if (pg + 1 < np) so[pg + 1] = acc[1];
-        }
       }
     }
     cp_wait<0>();
   }
-}
-
-// The same filter with one continuous ring per warp across its items: the
-// first tile of the next item is issued while the last tile of the current
-// one is consumed (the next item is fetched one tile before it is needed, so a
-// warp never holds more than one item ahead), instead of draining the ring at
-// every item boundary.  16-page tiles, 2 stages (the kernel above's layout).
-struct FlowItem {
-  int unit, p0, np, b, h;
-  const uint8_t* src0;
-  const uint8_t* src1;
-};
-
-template <int G>
-__global__ void __launch_bounds__(kQfWarps * 32) quest_filter_flow_kernel(tw_paged_kv kv,
-                                                                          const __nv_bfloat16* __restrict__ q,
-                                                                          float* __restrict__ scores, int max_chunks,
-                                                                          uint32_t* __restrict__ ctr, int item,
-                                                                          const __nv_bfloat16* __restrict__ k_new,
-                                                                          const __nv_bfloat16* __restrict__ v_new,
-                                                                          const int32_t* positions) {
-  pdl_wait();
-  pdl_trigger();
-  constexpr int kTileP = 16, kSt = 2;
-  extern __shared__ __align__(128) uint8_t qm_ring[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int t = lane & 3, r = lane >> 2, q8 = lane >> 3, rr = lane & 7;
-  const int units = kv.num_seqs * kv.num_kv_heads;
-  const int total = units * max_chunks;
-  uint8_t (*R)[kTileP * 512] = reinterpret_cast<uint8_t (*)[kTileP * 512]>(qm_ring + (size_t)warp * kSt * kTileP * 512);
-  const uint8_t* meta = reinterpret_cast<const uint8_t*>(kv.kmeta);
-  // next non-empty item (chunks in reverse: the open page's item first), with its
-  // page-table lookups; the item holding the open page appends the new row first
-  auto next_item = [&](FlowItem& f) -> bool {
-    for (int it = warp_fetch(ctr); it < total; it = warp_fetch(ctr)) {
-      const int unit = it % units;
-      const int p0 = (max_chunks - 1 - it / units) * item;
-      const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
-      const int pos = positions ? __ldg(positions + b) : -1;
-      const int n = positions ? min(pos + 1, kv.max_pages * kPage) : kv.seq_lens[b];
-      const int npages = (n + kPage - 1) / kPage;
-      if (p0 >= npages) continue;
-      const int np = min(item, npages - p0);
-      if (positions && npages - 1 < p0 + np) {
-        switch (kv.bits) {
-          case 2: append_row_warp<__nv_bfloat16, 2>(kv, b, h, lane, k_new, v_new, pos); break;
-          case 8: append_row_warp<__nv_bfloat16, 8>(kv, b, h, lane, k_new, v_new, pos); break;
-          default: append_row_warp<__nv_bfloat16, 4>(kv, b, h, lane, k_new, v_new, pos); break;
-        }
-        if (h == 0 && lane == 0 && pos < kv.max_pages * kPage) kv.seq_lens[b] = n;
-        __threadfence();  // the metadata stores precede this warp's cp.async reads of the page
-        __syncwarp();
-      }
-      const int* pt = kv.page_table + (size_t)b * kv.max_pages;
-      f.unit = unit; f.p0 = p0; f.np = np; f.b = b; f.h = h;
-      f.src0 = meta + (lane < np ? ((size_t)__ldg(pt + p0 + lane) * kv.num_kv_heads + h) * 512 : 0);
-      f.src1 = meta + (lane + 32 < np ? ((size_t)__ldg(pt + p0 + 32 + lane) * kv.num_kv_heads + h) * 512 : 0);
-      return true;
-    }
-    return false;
-  };
-  auto issue = [&](const FlowItem& f, int s, int slot) {
-    uint8_t* dst = R[slot];
-#pragma unroll 4
-    for (int i = 0; i < kTileP; ++i) {
-      const int pg = kTileP * s + i;
-      if (pg < f.np) {
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(
-            __shfl_sync(0xffffffffu, (unsigned long long)(pg < 32 ? f.src0 : f.src1), pg & 31));
-        cp_async16(dst + i * 512 + ((lane ^ (i & 7)) << 4), src + 16 * lane);
-      }
-    }
-  };
-  uint32_t qb[16][2];  // B fragments of [qneg ; qpos] for head column r
-  int cur_unit = -1;
-  FlowItem cur, nxt;
-  bool have = next_item(cur);
-  int g = 0;  // global tile counter: ring slot g % kSt
-  if (have) issue(cur, 0, 0);
-  cp_commit();
-  while (have) {
-    if (cur.unit != cur_unit) {
-      const uint32_t* qw =
-          reinterpret_cast<const uint32_t*>(q + ((size_t)cur.unit * G + (r < G ? r : 0)) * kHeadDim);
-      uint32_t w[8][2];
-#pragma unroll
-      for (int k8 = 0; k8 < 8; ++k8) {
-        w[k8][0] = r < G ? __ldg(qw + 8 * k8 + t) : 0u;
-        w[k8][1] = r < G ? __ldg(qw + 8 * k8 + t + 4) : 0u;
-      }
-      const __nv_bfloat162 zero2 = __float2bfloat162_rn(0.f);
-#pragma unroll
-      for (int k8 = 0; k8 < 8; ++k8) {
-#pragma unroll
-        for (int hb = 0; hb < 2; ++hb) {
-          const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&w[k8][hb]);
-          const __nv_bfloat162 neg = __hmin2(v, zero2), pos = __hmax2(v, zero2);
-          qb[k8][hb] = *reinterpret_cast<const uint32_t*>(&neg);
-          qb[k8 + 8][hb] = *reinterpret_cast<const uint32_t*>(&pos);
-        }
-      }
-      cur_unit = cur.unit;
-    }
-    const int ntile = (cur.np + kTileP - 1) / kTileP;
-    bool more = false;
-    for (int s = 0; s < ntile; ++s, ++g) {
-      if (s + 1 < ntile) {
-        issue(cur, s + 1, (g + 1) % kSt);
-      } else {
-        more = next_item(nxt);
-        if (more) issue(nxt, 0, (g + 1) % kSt);
-      }
-      cp_commit();
-      cp_wait<kSt - 1>();
-      __syncwarp();
-      const uint8_t* tile = R[g % kSt];
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      const int row = (q8 & 1) * 8 + rr;
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        uint32_t a[4];
-        const int chunk = 2 * kk + (q8 >> 1);
-        ldsm_x4_q(a, tile + row * 512 + ((chunk ^ (row & 7)) << 4));
-        mma_bf16_q(acc, a, qb[kk][0], qb[kk][1]);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int pg = kTileP * s + r + (e >= 2 ? 8 : 0);
-        const int gg = 2 * t + (e & 1);
-        if (gg < G && pg < cur.np) scores[((size_t)cur.unit * G + gg) * kv.max_pages + cur.p0 + pg] = acc[e];
-      }
-    }
-    have = more;
-    if (more) cur = nxt;
-  }
-  cp_wait<0>();
 }
 
 // tw_quest_scores: grid (ceil(max_pages/8), B*H_kv*G), 8 warps, warp per page.
@@ -512,13 +348,11 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
                    buf->page_scores, max_chunks, buf->counters + 2, item, (const __nv_bfloat16*)k_new,
                    (const __nv_bfloat16*)v_new, positions);
       };
-      // the continuous-ring variant is opt-in: measured slower (C2 K2 50.7 -> 55.3 us, r02)
-      static const bool flow = kQmTile == 16 && kQmStages == 2 && getenv("TW_QF_FLOW") && atoi(getenv("TW_QF_FLOW"));
       switch (kv->group_size) {
-        case 1: flow ? gom(quest_filter_flow_kernel<1>) : gom(quest_filter_mma_kernel<1>); break;
-        case 2: flow ? gom(quest_filter_flow_kernel<2>) : gom(quest_filter_mma_kernel<2>); break;
-        case 4: flow ? gom(quest_filter_flow_kernel<4>) : gom(quest_filter_mma_kernel<4>); break;
-        case 8: flow ? gom(quest_filter_flow_kernel<8>) : gom(quest_filter_mma_kernel<8>); break;
+        case 1: gom(quest_filter_mma_kernel<1>); break;
+        case 2: gom(quest_filter_mma_kernel<2>); break;
+        case 4: gom(quest_filter_mma_kernel<4>); break;
+        case 8: gom(quest_filter_mma_kernel<8>); break;
         default: return TW_ERR_INVALID;
       }
     } else {
