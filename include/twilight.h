@@ -115,7 +115,7 @@ typedef struct tw_decode_buffers {
   int32_t* final_count;     /* [U] */
   int32_t* unit_items;      /* [U][2]            first work item, number of work items */
   int32_t* work_items;      /* [max_items][2]    (unit, first token slot) */
-  uint32_t* counters;       /* [8]               device-side counters (zeroed by tw_select) */
+  uint32_t* counters;       /* [8]               device-side counters (zeroed by tw_select; [6] = max candidate pages) */
   float* partials;          /* [max_items][G][d+2] split-KV partial (o[d], m, l) */
   uint32_t* head_page_bits; /* optional [Hq][ceil(max_pages/32)] per-head Quest page sets */
   uint32_t* sel_bits;       /* [U][ceil(T/32)]   group-union bitmap over candidate positions */

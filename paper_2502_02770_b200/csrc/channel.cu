@@ -177,7 +177,10 @@ __global__ void __launch_bounds__(kChanThreads) chan_select_kernel(tw_paged_kv k
     if (has) out[base + incl - 1] = p;
     base += total;
   }
-  if (tid == 0) buf.cand_count[unit] = (int)base;
+  if (tid == 0) {
+    buf.cand_count[unit] = (int)base;
+    atomicMax(buf.counters + 6, base);  // the estimate's item range
+  }
 }
 
 }  // namespace tw

@@ -197,6 +197,7 @@ __device__ __forceinline__ int warp_fetch(uint32_t* ctr) {
   return __shfl_sync(0xffffffffu, it, 0);
 }
 
+
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }

@@ -99,7 +99,10 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
     }
     }
   };
-  for (int it = warp_fetch(buf.counters + 3); it < units * max_chunks; it = warp_fetch(buf.counters + 3)) {
+  // chunks past the longest candidate list are empty: the select left the
+  // maximum candidate-page count in counters[6]
+  const int live_chunks = min(max_chunks, ((int)buf.counters[6] + item - 1) / item);
+  for (int it = warp_fetch(buf.counters + 3); it < units * live_chunks; it = warp_fetch(buf.counters + 3)) {
     const int unit = it % units;  // chunk-major: non-empty items come first, spread over all warps
     const int c0 = (it / units) * item;
     const int ncand = buf.cand_count[unit];

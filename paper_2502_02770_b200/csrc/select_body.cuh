@@ -235,13 +235,19 @@ __device__ __forceinline__ void select_unit_body(const int unit, const tw_paged_
   int* out = buf.cand_pages + (size_t)unit * Pmax;
   if (all) {  // every page: no bitmap
     for (int i = threadIdx.x; i < P; i += blockDim.x) out[i] = i;
-    if (threadIdx.x == 0) buf.cand_count[unit] = P;
+    if (threadIdx.x == 0) {
+      buf.cand_count[unit] = P;
+      atomicMax(buf.counters + 6, (uint32_t)P);  // the estimate's item range
+    }
     return;
   }
   if (sw) {  // two page ranges
     const int nb = P - sw_b;
     for (int i = threadIdx.x; i < sw_a + nb; i += blockDim.x) out[i] = i < sw_a ? i : sw_b + (i - sw_a);
-    if (threadIdx.x == 0) buf.cand_count[unit] = sw_a + nb;
+    if (threadIdx.x == 0) {
+      buf.cand_count[unit] = sw_a + nb;
+      atomicMax(buf.counters + 6, (uint32_t)(sw_a + nb));
+    }
     return;
   }
   uint32_t base = 0;
@@ -259,7 +265,10 @@ __device__ __forceinline__ void select_unit_body(const int unit, const tw_paged_
     }
     base += total;
   }
-  if (threadIdx.x == 0) buf.cand_count[unit] = (int)base;
+  if (threadIdx.x == 0) {
+    buf.cand_count[unit] = (int)base;
+    atomicMax(buf.counters + 6, base);
+  }
   STRACE();
 }
 
