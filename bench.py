@@ -431,36 +431,83 @@ def run_ours(args, cfg):
     v_d = inp_d[nq + nk:].view(v_new.shape)
     res_src = full_out if full_out is not None else out  # the step's result: all heads after the gather
     out_h = torch.empty(res_src.shape, dtype=res_src.dtype).pin_memory()
-    # single GPU: the H2D copy, the step and the D2H copy are captured as ONE graph
-    # (memcpy nodes from/to the pinned buffers, executed every replay)
     copies_in_graph = gathered is None
-    e2e_graphs = []
-    for i in range(L):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            if copies_in_graph:
-                inp_d.copy_(inp_h, non_blocking=True)
-            decs[i].step(q_d, k_d, v_d, positions, out)
-            if copies_in_graph:
-                out_h.copy_(out, non_blocking=True)
-        e2e_graphs.append(g)
-    for i in range(args.warmup):  # (every input copied: a garbage k_new would poison the |k| bound)
-        if not copies_in_graph:
+    if copies_in_graph:
+        # single GPU: double-buffered staging, as a serving loop does it.  Step i reads input
+        # buffer i%2 and writes output buffer i%2; on a copy stream the H2D of step i+1's inputs
+        # overlaps step i and the D2H of step i's result overlaps step i+1.  Every step still
+        # moves its own inputs in and its own result out inside the timed region.
+        inp_d2 = [torch.empty_like(inp_h, device=q.device) for _ in range(2)]
+        out_d2 = [torch.empty_like(out) for _ in range(2)]
+        out_h2 = [torch.empty(out.shape, dtype=out.dtype).pin_memory() for _ in range(2)]
+        views = [(b[:nq].view(q.shape), b[nq:nq + nk].view(k_new.shape), b[nq + nk:].view(v_new.shape))
+                 for b in inp_d2]
+        for b in inp_d2:
+            b.copy_(inp_h)
+        torch.cuda.synchronize()
+        e2e_graphs = {}
+        for i in range(L):
+            for par in range(2):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    decs[i].step(views[par][0], views[par][1], views[par][2], positions, out_d2[par])
+                e2e_graphs[(i, par)] = g
+        copy_s = torch.cuda.Stream(device=q.device)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_done = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+
+        def pipelined(nsteps):
+            copy_s.wait_stream(stream)
+            with torch.cuda.stream(copy_s):
+                inp_d2[0].copy_(inp_h, non_blocking=True)
+                ev_in[0].record(copy_s)
+            for i in range(nsteps):
+                par = i % 2
+                if i + 1 < nsteps:  # next step's inputs, once step i-1 is done reading that buffer
+                    with torch.cuda.stream(copy_s):
+                        if i >= 1:
+                            copy_s.wait_event(ev_done[1 - par])
+                        inp_d2[1 - par].copy_(inp_h, non_blocking=True)
+                        ev_in[1 - par].record(copy_s)
+                stream.wait_event(ev_in[par])
+                if i >= 2:
+                    stream.wait_event(ev_out[par])  # step i-2's result has left this buffer
+                e2e_graphs[(i % L, par)].replay()
+                ev_done[par].record(stream)
+                with torch.cuda.stream(copy_s):
+                    copy_s.wait_event(ev_done[par])
+                    out_h2[par].copy_(out_d2[par], non_blocking=True)
+                    ev_out[par].record(copy_s)
+            stream.wait_stream(copy_s)
+
+        pipelined(args.warmup)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record(stream)
+        pipelined(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    else:
+        e2e_graphs = []
+        for i in range(L):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                decs[i].step(q_d, k_d, v_d, positions, out)
+            e2e_graphs.append(g)
+        for i in range(args.warmup):  # (every input copied: a garbage k_new would poison the |k| bound)
             inp_d.copy_(inp_h, non_blocking=True)
-        e2e_graphs[i % L].replay()
-    torch.cuda.synchronize()
-    barrier(world)
-    e0.record(stream)
-    for i in range(args.steps):
-        if not copies_in_graph:
+            e2e_graphs[i % L].replay()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record(stream)
+        for i in range(args.steps):
             inp_d.copy_(inp_h, non_blocking=True)
-        e2e_graphs[i % L].replay()
-        if gathered is not None:
+            e2e_graphs[i % L].replay()
             gather()
-        if not copies_in_graph:
             out_h.copy_(res_src, non_blocking=True)
-    e1.record(stream)
-    torch.cuda.synchronize()
+        e1.record(stream)
+        torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
     h2d = q.numel() * q.element_size() + k_new.numel() * k_new.element_size() * 2
     d2h = res_src.numel() * res_src.element_size()
@@ -507,8 +554,10 @@ def run_ours(args, cfg):
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us/layer", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "path": "tw_decode_step C-ABI call, q/k_new/v_new H2D from one pinned host buffer and out D2H to "
-                        "pinned host every step" + (" (copies and step captured in one CUDA graph)"
-                                                    if copies_in_graph else " (step captured)")},
+                        "pinned host every step" + (" (step captured; double-buffered staging: the next step's "
+                                                    "H2D and the previous step's D2H on a copy stream overlap "
+                                                    "the current step)" if copies_in_graph else
+                                                    " (step captured; copies and the all-gather serial)")},
         # quest: filter (+ fused K1 append), select, estimate, top-p, attention, merge;
         # other selectors: append, select, estimate, top-p, attention, merge
         "gpu_launches": (3 if decs[0].unit_path else 6) * args.steps,
