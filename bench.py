@@ -488,6 +488,25 @@ def run_ours(args, cfg):
         pipelined(args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
+        # the same with no overlap (H2D, step, D2H serial in one graph per layer), reported beside it
+        ser_graphs = []
+        for i in range(L):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                inp_d.copy_(inp_h, non_blocking=True)
+                decs[i].step(q_d, k_d, v_d, positions, out)
+                out_h.copy_(out, non_blocking=True)
+            ser_graphs.append(g)
+        for i in range(args.warmup):
+            ser_graphs[i % L].replay()
+        torch.cuda.synchronize()
+        es0, es1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        es0.record(stream)
+        for i in range(args.steps):
+            ser_graphs[i % L].replay()
+        es1.record(stream)
+        torch.cuda.synchronize()
+        e2e_serial_ms = es0.elapsed_time(es1) / args.steps
     else:
         e2e_graphs = []
         for i in range(L):
@@ -508,6 +527,7 @@ def run_ours(args, cfg):
             out_h.copy_(res_src, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
+        e2e_serial_ms = None
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
     h2d = q.numel() * q.element_size() + k_new.numel() * k_new.element_size() * 2
     d2h = res_src.numel() * res_src.element_size()
@@ -553,6 +573,9 @@ def run_ours(args, cfg):
                          "(K+V+INT4+meta >> 126 MB L2)", "cuda_graphs": True},
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us/layer", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
+                **({"serial_value": round(e2e_serial_ms * 1e3, 2),
+                    "serial_note": "copies and step serialised in one graph per layer (no overlap)"}
+                   if e2e_serial_ms is not None else {}),
                 "path": "tw_decode_step C-ABI call, q/k_new/v_new H2D from one pinned host buffer and out D2H to "
                         "pinned host every step" + (" (step captured; double-buffered staging: the next step's "
                                                     "H2D and the previous step's D2H on a copy stream overlap "
