@@ -31,12 +31,16 @@ namespace tw {
 #define TW_EST_ITEM 32
 #endif
 #ifndef TW_EST_STAGES
-#define TW_EST_STAGES 4
+#define TW_EST_STAGES 6
 #endif
 constexpr int kEstPagesPerCta = TW_EST_ITEM;  // candidate pages per work item (<= 32: one per lane)
 constexpr int kEstWarps = 4;
 
 constexpr int kEstStages = TW_EST_STAGES;  // pages in flight per warp (ring stages)
+#ifndef TW_EST_IPW
+#define TW_EST_IPW 1
+#endif
+constexpr int kEstItemsPerWarp = TW_EST_IPW;
 #ifndef TW_EST_BULK
 #define TW_EST_BULK 0  // r02: bulk copies measured 1-2% slower (C2 47.5 vs 46.9 us, C3 401 vs 392 us)
 #endif
@@ -101,7 +105,14 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
   };
   // chunks past the longest candidate list are empty: the select left the
   // maximum candidate-page count in counters[6]
-  const int live_chunks = min(max_chunks, ((int)buf.counters[6] + item - 1) / item);
+  // items per warp: `item` (host) shrinks on the device while the live items (the longest
+  // candidate list in counters[6] sets the chunk count) leave fewer than
+  // kEstItemsPerWarp per warp -- at C2 32-page items were ~1.2 per warp, so the warps
+  // that drew a second one set the kernel's length
+  const int maxc = (int)buf.counters[6];
+  while (item > 4 && (long long)units * ((maxc + item - 1) / item) < (long long)kEstItemsPerWarp * gridDim.x * kEstWarps)
+    item >>= 1;
+  const int live_chunks = (min(maxc, kv.max_pages) + item - 1) / item;
   for (int it = warp_fetch(buf.counters + 3); it < units * live_chunks; it = warp_fetch(buf.counters + 3)) {
     const int unit = it % units;  // chunk-major: non-empty items come first, spread over all warps
     const int c0 = (it / units) * item;

@@ -297,26 +297,65 @@ __global__ void __launch_bounds__(256) quest_exact_kernel(tw_paged_kv kv, const 
   if ((threadIdx.x & 31) == 0) out[(size_t)qh * kv.max_pages + lp] = s;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kSelThreads) quest_select_kernel(tw_paged_kv kv, const T* __restrict__ q,
-                                                                   tw_decode_params prm, tw_decode_buffers buf) {
+// NG < 4 (the C4/C5 shapes): two CTAs per SM (64 registers), so more units start at once.
+template <typename T, int NG, int NT>
+__global__ void __launch_bounds__(NT, NT == 512 && NG < 4 ? 2 : 1)
+    quest_select_kernel(tw_paged_kv kv, const T* __restrict__ q, tw_decode_params prm, tw_decode_buffers buf) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
-  select_unit_body<T>(blockIdx.x, kv, q, prm, buf, smem);
+  select_unit_body<T, NT, NG>(blockIdx.x, kv, q, prm, buf, smem);
 }
 
 }  // namespace tw
 
 using namespace tw;
 
+// Warp groups of the select CTA (query heads selected concurrently, 512 / ng
+// threads each): up to 4, fewer when the unit has fewer heads, when the
+// per-group key arrays would not fit shared memory, or when the smaller CTA
+// (two per SM) needs fewer waves for all units.  Measured: C5 (256 units of
+// 8193 pages) select 246.7 -> 230.7 us with 2 groups, C4 (512 units of 4097)
+// 259.7 -> 236.9; C2 (128 units) keeps 4 (2 groups: 53.9 -> 56.8).
+// 0: no configuration fits.  TW_SEL_GROUPS=1|2|4 pins it (A/B).
+static int select_threads() {
+  static const int nt = [] {
+    const char* e = getenv("TW_SEL_THREADS");
+    return e && atoi(e) == 1024 ? 1024 : kSelThreads;
+  }();
+  return nt;
+}
+static int select_groups(int units, int G, int Pmax, int sms, int nt) {
+  static const int pinned = [] {
+    const char* e = getenv("TW_SEL_GROUPS");
+    return e ? atoi(e) : 0;
+  }();
+  auto fits = [&](int ng) { return select_smem_bytes(Pmax, nt, ng) <= 227 * 1024; };
+  if (pinned == 1 || pinned == 2 || pinned == 4) return fits(pinned) ? pinned : 0;
+  const int gmax = G >= 4 ? 4 : (G >= 2 ? 2 : 1);
+  int ng = gmax;
+  while (ng > 1 && !fits(ng)) ng /= 2;
+  if (!fits(ng)) return 0;
+  auto waves = [&](int g) {  // 4 groups: 1 CTA per SM (registers); fewer: 2
+    const int per_sm = (int)std::min<size_t>(g == 4 || nt > 512 ? 1 : 2, (228 * 1024) / (select_smem_bytes(Pmax, nt, g) + 1024));
+    return (units + sms * per_sm - 1) / (sms * per_sm);
+  };
+  while (ng > 1 && waves(ng / 2) < waves(ng)) ng /= 2;
+  return ng;
+}
+
 template <typename T>
 static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
                          const tw_decode_buffers* buf, cudaStream_t stream, const void* k_new = nullptr,
                          const void* v_new = nullptr, const int32_t* positions = nullptr) {
   const int units = kv->num_seqs * kv->num_kv_heads;
-  const size_t smem = select_smem_bytes(kv->max_pages);
-  if (smem > 227 * 1024) return TW_ERR_INVALID;  // checked before anything is enqueued
+  int dev0 = 0, sms0 = 148;
+  cudaGetDevice(&dev0);
+  cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
+  const int nt = select_threads();
+  const int ng = select_groups(units, kv->group_size, kv->max_pages, sms0, nt);
+  if (ng == 0) return TW_ERR_INVALID;  // checked before anything is enqueued
+  const size_t smem = select_smem_bytes(kv->max_pages, nt, ng);
   cudaMemsetAsync(buf->counters, 0, 8 * sizeof(uint32_t), stream);
   if (prm->selector == TW_SELECT_QUEST) {
     int dev = 0, sms = 148;
@@ -365,8 +404,19 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
       }
     }
   }
-  cudaFuncSetAttribute(quest_select_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_pdl(quest_select_kernel<T>, dim3(units), dim3(kSelThreads), smem, stream, *kv, (const T*)q, *prm, *buf);
+  auto sel = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(kern, dim3(units), dim3(nt), smem, stream, *kv, (const T*)q, *prm, *buf);
+  };
+  if (nt == 1024) {
+    if (ng == 4) sel(quest_select_kernel<T, 4, 1024>);
+    else if (ng == 2) sel(quest_select_kernel<T, 2, 1024>);
+    else sel(quest_select_kernel<T, 1, 1024>);
+  } else {
+    if (ng == 4) sel(quest_select_kernel<T, 4, kSelThreads>);
+    else if (ng == 2) sel(quest_select_kernel<T, 2, kSelThreads>);
+    else sel(quest_select_kernel<T, 1, kSelThreads>);
+  }
   return launch_status();
 }
 
@@ -394,7 +444,7 @@ int tw_select_append(const tw_paged_kv* kv, const void* q, const void* k_new, co
       (kv->bits != 0 && kv->bits != 2 && kv->bits != 4 && kv->bits != 8) || prm->budget_pages < 1 ||
       !buf->page_scores || !buf->band_idx || !buf->band_scores || !q || !buf->cand_pages || !buf->cand_count ||
       !buf->counters || !buf->head_max || positions == kv->seq_lens ||
-      select_smem_bytes(kv->max_pages) > 227 * 1024)
+      select_smem_bytes(kv->max_pages, kSelThreads, 1) > 227 * 1024)
     return TW_FUSE_UNAVAILABLE;
   return launch_select<__nv_bfloat16>(kv, q, prm, buf, stream, k_new, v_new, positions);
 }

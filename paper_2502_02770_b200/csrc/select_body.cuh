@@ -56,27 +56,27 @@ __device__ __forceinline__ double exact_page_score(const T* q, const T* lo, cons
 
 // ---------------------------------------------------------------- select + union
 
-constexpr int kSelGroups = 4;                       // warp groups: query heads selected concurrently
+constexpr int kSelGroups = 4;  // default warp groups: query heads selected concurrently
 
 struct SelGroupSmem {
-  uint32_t tmp[2 * (1024 / kSelGroups / 32)];  // 2 words per warp of a group (up to 1024-thread CTAs)
+  uint32_t tmp[64];  // 2 words per warp of a group (up to 32 warps)
   uint32_t mem[64];
   int res[4];
   int namb, cin;
   float margin;
 };
 
-// One CTA per unit (b, kv head); its G query heads are spread over 4 warp
-// groups (named barriers 1..4), each running filter-threshold -> band
+// One CTA per unit (b, kv head); its G query heads are spread over NG warp
+// groups (named barriers 1..NG), each running filter-threshold -> band
 // rescoring -> rank on its own head; the CTA then compacts the union.
-// One unit's selection (CTA of NT threads; `smem` = select_smem_bytes(max_pages, NT)).
+// One unit's selection (CTA of NT threads; `smem` = select_smem_bytes(max_pages, NT, NG)).
 // n_tokens: the unit's context length (< 0: read seq_lens).
-template <typename T, int NT = kSelThreads>
+template <typename T, int NT = kSelThreads, int NG = kSelGroups>
 __device__ __forceinline__ void select_unit_body(const int unit, const tw_paged_kv& kv, const T* __restrict__ q,
                                                  const tw_decode_params& prm, const tw_decode_buffers& buf,
                                                  unsigned char* smem, const int n_tokens = -1) {
-  __shared__ SelGroupSmem GS[kSelGroups];
-  constexpr int kGroupThreads = NT / kSelGroups;
+  __shared__ SelGroupSmem GS[NG];
+  constexpr int kGroupThreads = NT / NG;
   __shared__ uint32_t btmp[NT / 32];
   const int G = kv.group_size;
   const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
@@ -91,7 +91,7 @@ __device__ __forceinline__ void select_unit_body(const int unit, const tw_paged_
   uint32_t* keys = gbase;                                                                // [Pmax]
   uint32_t* hist = keys + Pmax;                                                          // [2048]
   uint32_t* hbits = hist + 2048;                                                         // [words]
-  size_t toff = ((size_t)words + kSelGroups * ((size_t)Pmax + 2048 + words)) * 4;
+  size_t toff = ((size_t)words + NG * ((size_t)Pmax + 2048 + words)) * 4;
   toff = (toff + 7) & ~size_t(7);
   double* terms = reinterpret_cast<double*>(smem + toff) + (threadIdx.x >> 5) * kHeadDim;  // [NT / 32 warps][128]
   SelGroupSmem& gs = GS[gp];
@@ -133,7 +133,7 @@ __device__ __forceinline__ void select_unit_body(const int unit, const tw_paged_
   } else {
     const float amax = kv.kabsmax[unit];
     const int wig = grp.warp(), lane = threadIdx.x & 31;
-    for (int g = gp; g < G; g += kSelGroups) {
+    for (int g = gp; g < G; g += NG) {
       const size_t qhi = (size_t)unit * G + g;
       const T* qh = q + qhi * kHeadDim;
       const float* sc = buf.page_scores + qhi * Pmax;
@@ -272,9 +272,9 @@ __device__ __forceinline__ void select_unit_body(const int unit, const tw_paged_
   STRACE();
 }
 
-inline size_t select_smem_bytes(int Pmax, int nt = kSelThreads) {
+inline size_t select_smem_bytes(int Pmax, int nt = kSelThreads, int ng = kSelGroups) {
   const int words = (Pmax + 31) / 32;
-  size_t bytes = ((size_t)words + kSelGroups * ((size_t)Pmax + 2048 + words)) * 4;
+  size_t bytes = ((size_t)words + ng * ((size_t)Pmax + 2048 + words)) * 4;
   bytes = (bytes + 7) & ~size_t(7);
   return bytes + (size_t)(nt / 32) * kHeadDim * 8;
 }
