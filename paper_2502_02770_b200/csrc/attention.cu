@@ -117,6 +117,23 @@ __device__ __forceinline__ void issue_stage(WarpSmem<T>& W, const tw_paged_kv& k
   }
 }
 
+#ifdef TW_ATT_TRACE
+// per work item: start, end (globaltimer ns), global warp id (tools/att_trace.py)
+static __device__ unsigned long long g_at[32768][3];
+extern "C" int tw_debug_atrace(unsigned long long* host_out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host_out, g_at, sizeof(g_at));
+  static unsigned long long zeros[32768 * 3];
+  cudaMemcpyToSymbol(g_at, zeros, sizeof(zeros));
+  return 0;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 // ------------------------------------------------------------------ bf16 consumer (tensor cores)
 
 struct StateMMA {
@@ -279,6 +296,9 @@ __global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const
   for (int it = warp_fetch(ctr); it < nitems_total; it = warp_fetch(ctr)) {
     const ItemDesc d = get_item<DENSE>(kv, buf, it, chunk, max_chunks);
     if (d.count <= 0) continue;
+#ifdef TW_ATT_TRACE
+    if (lane == 0 && it < 32768) { g_at[it][0] = gtimer(); g_at[it][2] = gw; }
+#endif
     const int b = d.unit / H, h = d.unit % H;
     // Row indices (token id -> page table -> row): the first 32 rows (the
     // ring's first stages) are resolved first and their copies issued, then
@@ -450,6 +470,9 @@ __global__ void __launch_bounds__(kAttThreads) attn_kernel(tw_paged_kv kv, const
       }
     }
     cp_wait<0>();
+#ifdef TW_ATT_TRACE
+    if (lane == 0 && it < 32768) g_at[it][1] = gtimer();
+#endif
   }
   // units whose final set is empty: zeros (sparse_attention, attention.py:126-129)
   if (!DENSE) {
