@@ -27,6 +27,23 @@
 
 namespace tw {
 
+#ifdef TW_EST_TRACE
+// per work item: start, end (globaltimer ns), global warp id (tools/att_trace.py --kernel estimate)
+static __device__ unsigned long long g_et[65536][3];
+extern "C" int tw_debug_etrace(unsigned long long* host_out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host_out, g_et, sizeof(g_et));
+  static unsigned long long zeros[65536 * 3];
+  cudaMemcpyToSymbol(g_et, zeros, sizeof(zeros));
+  return 0;
+}
+__device__ __forceinline__ unsigned long long etimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 #ifndef TW_EST_ITEM
 #define TW_EST_ITEM 32
 #endif
@@ -118,6 +135,9 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
     const int c0 = (it / units) * item;
     const int ncand = buf.cand_count[unit];
     if (c0 >= ncand) continue;
+#ifdef TW_EST_TRACE
+    if (lane == 0 && it < 65536) { g_et[it][0] = etimer(); g_et[it][2] = blockIdx.x * kEstWarps + warp; }
+#endif
     const int b = unit / kv.num_kv_heads, h = unit % kv.num_kv_heads;
     const int n = kv.seq_lens[b];
     const int np = min(item, ncand - c0);
@@ -282,6 +302,9 @@ __global__ void __launch_bounds__(kEstWarps * 32) estimate_kernel(tw_paged_kv kv
     issued = base + np;  // every issued page was waited on above
 #else
     cp_wait<0>();
+#endif
+#ifdef TW_EST_TRACE
+    if (lane == 0 && it < 65536) g_et[it][1] = etimer();
 #endif
   }
   if (cur_unit >= 0) flush_max(cur_unit);

@@ -311,6 +311,18 @@ __global__ void __launch_bounds__(NT, NT == 512 && NG < 4 ? 2 : 1)
 
 using namespace tw;
 
+#ifdef TW_TOPP_TRACE
+extern "C" int tw_debug_select_strace(unsigned long long* host_out) {  // quest_select_kernel's phase stamps
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host_out, g_strace, sizeof(g_strace));
+  int zeros[512] = {0};
+  cudaMemcpyToSymbol(g_strace_phase, zeros, sizeof(zeros));
+  static unsigned long long z2[512 * 16];
+  cudaMemcpyToSymbol(g_strace, z2, sizeof(z2));
+  return 0;
+}
+#endif
+
 // Warp groups of the select CTA (query heads selected concurrently, 512 / ng
 // threads each): up to 4, fewer when the unit has fewer heads, when the
 // per-group key arrays would not fit shared memory, or when the smaller CTA

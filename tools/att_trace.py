@@ -1,4 +1,5 @@
-"""Work-item timeline of the sparse attention (K4) from a library built with
+"""Work-item timeline of the sparse attention (K4; or, with --kernel estimate
+and -DTW_EST_TRACE, the INT4 estimate K3a) from a library built with
 -DTW_ATT_TRACE:
     tools/build_variant.sh atrace -DTW_ATT_TRACE
     TW_LIB_PATH=tools/_variants/atrace/libtwilight.so python tools/att_trace.py --config C2
@@ -24,6 +25,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--chunk", type=int, default=0)
 ap.add_argument("--json", default=None)
+ap.add_argument("--kernel", default="attention", choices=["attention", "estimate"])
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 B, H, G, n = cfg["B"], cfg["H"], cfg["G"], cfg["n"]
@@ -37,23 +39,26 @@ dec = TwilightDecoder(cache, cfg["selector"], budget=cfg["budget"], p=cfg["p"], 
 q = step.q.contiguous()
 k_new, v_new = step.k_new.contiguous(), step.v_new.contiguous()
 positions = torch.full((B,), n - 1, dtype=torch.int32, device="cuda")
-buf = (ctypes.c_ulonglong * (32768 * 3))()
-if not hasattr(_lib.lib(), "tw_debug_atrace"):
-    sys.exit("library built without -DTW_ATT_TRACE")
+NMAX = 32768 if args.kernel == "attention" else 65536
+buf = (ctypes.c_ulonglong * (NMAX * 3))()
+dbg = "tw_debug_atrace" if args.kernel == "attention" else "tw_debug_etrace"
+if not hasattr(_lib.lib(), dbg):
+    sys.exit("library built without -DTW_ATT_TRACE / -DTW_EST_TRACE")
 res = {}
 for rep in range(3):
     dec.step(q, k_new, v_new, positions=positions)
     torch.cuda.synchronize()
-    _lib.lib().tw_debug_atrace(buf)
-a = np.frombuffer(buf, dtype=np.uint64).reshape(32768, 3).astype(np.int64)
+    getattr(_lib.lib(), dbg)(buf)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(NMAX, 3).astype(np.int64)
 a = a[a[:, 0] > 0]
 t0 = a[:, 0].min()
 st, en = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3
 span = float(en.max())
 grid = np.linspace(0, span, 41)
 busy = [int(((st <= t) & (en > t)).sum()) for t in grid]
+nwarps = len(np.unique(a[:, 2]))
 dur = en - st
-res = {"config": args.config, "chunk": dec.params.chunk_tokens, "items": int(len(a)),
+res = {"config": args.config, "kernel": args.kernel, "chunk": dec.params.chunk_tokens, "items": int(len(a)),
        "warps": int(len(np.unique(a[:, 2]))), "span_us": round(span, 2),
        "first_start_spread_us": round(float(np.sort(st)[min(len(st) - 1, len(np.unique(a[:, 2])) - 1)]), 2),
        "last_start_us": round(float(st.max()), 2), "tail_us": round(span - float(st.max()), 2),
