@@ -25,7 +25,7 @@ done
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches_${TAG}_C2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 python tools/launches.py gpurun_out/launches_${TAG}_C2.csv --json gpurun_out/launches_${TAG}_C2.json | grep "tw::" || true
-for c in C1 C2 C3 C5; do
+for c in C1 C2 C3 C5 C4; do
   timeout 900 ncu --set full --import-source on --clock-control none \
     -k regex:"attn_kernel|quest_select|topp_unit|topp_head|estimate_kernel|quest_filter|append_kernel|merge_kernel|unit_step" -c 8 \
     -o /tmp/full_${TAG}_$c python tools/prof_step.py --config $c --reps 1 > /dev/null 2>&1
