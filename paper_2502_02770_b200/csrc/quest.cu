@@ -133,13 +133,23 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_kernel(tw_paged_kv
 //   score = qneg . lo + qpos . hi,  qpos = max(q, 0), qneg = min(q, 0),
 // i.e. a [pages x 256] x [256 x heads] product -> legacy mma.sync m16n8k16
 // (bf16 products exact, fp32 accumulation, covered by the select margin).
-// Per warp: 16-page tiles (16 x 512 B, XOR-swizzled rows) through a TW_QM_STAGES-deep (2)
-// cp.async ring; one ldmatrix.x4 + one MMA per page-tile k-step.
+// Per warp: 16-page tiles through a TW_QM_STAGES-deep (2) ring of TMA bulk
+// copies (below); one ldmatrix.x4 + one MMA per page-tile k-step.
 #ifndef TW_QM_STAGES
 #define TW_QM_STAGES 2
 #endif
 constexpr int kQmStages = TW_QM_STAGES;
 constexpr int kQmTile = 16;  // pages per stage (= the MMA's rows)
+// Every page is ONE TMA bulk copy (cp.async.bulk, issued by the lane holding
+// its address) into a row padded to 528 B (bulk copies cannot swizzle; the pad
+// keeps ldmatrix's 8 rows in different banks), completing on a per-stage
+// mbarrier (measured: C2 K2 49.4 -> 48.8 us, step 282.5 -> 280.5 us; C4 K2
+// 246 -> 237 us).  TW_QF_BULK=0: 32 LDGSTS of 16 B per page into swizzled rows.
+#ifndef TW_QF_BULK
+#define TW_QF_BULK 1
+#endif
+constexpr int kQmRow = TW_QF_BULK ? 528 : 512;
+constexpr int kQmStageBytes = kQmTile * kQmRow;
 
 __device__ __forceinline__ void ldsm_x4_q(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -171,8 +181,15 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane & 3, r = lane >> 2, q8 = lane >> 3, rr = lane & 7;
   const int units = kv.num_seqs * kv.num_kv_heads;
-  uint8_t (*R)[kQmTile * 512] =
-      reinterpret_cast<uint8_t (*)[kQmTile * 512]>(qm_ring + (size_t)warp * kQmStages * kQmTile * 512);
+  uint8_t (*R)[kQmStageBytes] =
+      reinterpret_cast<uint8_t (*)[kQmStageBytes]>(qm_ring + (size_t)warp * kQmStages * kQmStageBytes);
+#if TW_QF_BULK
+  __shared__ __align__(8) uint64_t qbars[kQfWarps][kQmStages];
+  if (lane < kQmStages) mbar_init(&qbars[warp][lane], 1);
+  mbar_fence_init();
+  __syncwarp();
+  uint32_t issued = 0;  // tiles this warp has issued: tile j of all items uses slot j % stages, parity (j / stages) & 1
+#endif
   uint32_t qb[16][2];  // B fragments of [qneg ; qpos] for head column r
   int cur_unit = -1;
   for (int it = warp_fetch(ctr); it < units * max_chunks; it = warp_fetch(ctr)) {
@@ -195,6 +212,9 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
       if (h == 0 && lane == 0 && pos < kv.max_pages * kPage)
         kv.seq_lens[b] = n;  // every reader in this kernel uses positions
       __threadfence();  // the metadata stores precede this warp's cp.async reads of the page
+#if TW_QF_BULK
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // ... and its bulk (async-proxy) reads
+#endif
       __syncwarp();
     }
     const int* pt = kv.page_table + (size_t)b * kv.max_pages;
@@ -204,6 +224,20 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
     if (lane < np) src0 += ((size_t)pt[p0 + lane] * kv.num_kv_heads + h) * 512;
     if (lane + 32 < np) src1 += ((size_t)pt[p0 + 32 + lane] * kv.num_kv_heads + h) * 512;
     const int ntile = (np + kQmTile - 1) / kQmTile;
+#if TW_QF_BULK
+    const uint32_t tbase = issued;
+    auto issue = [&](int s) {  // tile s = pages 16s .. 16s+15, held by lanes 16(s&1) + x of src0 (s < 2) / src1
+      const uint32_t slot = (tbase + s) % kQmStages;
+      const int cnt = min(kQmTile, np - kQmTile * s);
+      if (lane == 0) mbar_arrive_expect_tx(&qbars[warp][slot], cnt * 512);
+      __syncwarp();
+      const int x = lane - 16 * (s & 1);
+      if (x >= 0 && x < cnt) bulk_g2s(R[slot] + x * kQmRow, s >= 2 ? src1 : src0, 512, &qbars[warp][slot]);
+    };
+#pragma unroll
+    for (int s = 0; s < kQmStages - 1; ++s)
+      if (s < ntile) issue(s);
+#else
     auto issue = [&](int s) {
       uint8_t* dst = R[s % kQmStages];
 #pragma unroll 4
@@ -222,6 +256,7 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
       if (s < ntile) issue(s);
       cp_commit();
     }
+#endif
     if (unit != cur_unit) {
       // k = 16kk + {2t, 2t+1 | 2t+8, 2t+9}; k < 128 -> qneg[k], else qpos[k - 128]:
       // the bf16 pair (c, c+1), c = k & 127, is 32-bit word 8(kk & 7) + t + 4hb of the head's row
@@ -247,10 +282,16 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
     }
     for (int s = 0; s < ntile; ++s) {
       if (s + kQmStages - 1 < ntile) issue(s + kQmStages - 1);
+#if TW_QF_BULK
+      const uint32_t slot = (tbase + s) % kQmStages;
+      mbar_wait(&qbars[warp][slot], ((tbase + s) / kQmStages) & 1);
+      const uint8_t* tile = R[slot];
+#else
       cp_commit();
       cp_wait<kQmStages - 1>();
       __syncwarp();
       const uint8_t* tile = R[s % kQmStages];
+#endif
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
       {
         const int row = (q8 & 1) * 8 + rr;
@@ -258,7 +299,11 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
         for (int kk = 0; kk < 16; ++kk) {
           uint32_t a[4];
           const int chunk = 2 * kk + (q8 >> 1);
+#if TW_QF_BULK
+          ldsm_x4_q(a, tile + row * kQmRow + (chunk << 4));
+#else
           ldsm_x4_q(a, tile + row * 512 + ((chunk ^ (row & 7)) << 4));
+#endif
           mma_bf16_q(acc, a, qb[kk][0], qb[kk][1]);
         }
         __syncwarp();
@@ -271,7 +316,11 @@ __global__ void __launch_bounds__(kQfWarps * 32) quest_filter_mma_kernel(tw_page
         }
       }
     }
+#if TW_QF_BULK
+    issued = tbase + ntile;  // every issued tile was waited on above
+#else
     cp_wait<0>();
+#endif
   }
 }
 
@@ -389,7 +438,7 @@ static int launch_select(const tw_paged_kv* kv, const void* q, const tw_decode_p
     };
     if constexpr (sizeof(T) == 2) {
       auto gom = [&](auto kern) {
-        const int smem = kQfWarps * kQmStages * kQmTile * 512;
+        const int smem = kQfWarps * kQmStages * kQmStageBytes;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQfWarps * 32, smem);
