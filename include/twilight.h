@@ -185,6 +185,13 @@ int tw_topp(const tw_paged_kv* kv, const tw_decode_params* prm, const tw_decode_
 int tw_sparse_attention(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
                         const tw_decode_buffers* buf, float* out, cudaStream_t stream);
 
+/* tw_sparse_attention in parts, for per-kernel timing: part 1 launches only
+ * the gather / subset-softmax kernel (split units' partials are left in
+ * buf->partials, their out rows unwritten), part 2 only the split-KV merge;
+ * 0 = both (= tw_sparse_attention). */
+int tw_sparse_attention_part(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
+                             const tw_decode_buffers* buf, float* out, int32_t part, cudaStream_t stream);
+
 /* K5 -- dense paged decode attention over all seq_lens[b] tokens (the bypass
  * layers' path, bypass_config pipeline.py:129-136; the speedup baseline). */
 int tw_dense_attention(const tw_paged_kv* kv, const void* q, const tw_decode_buffers* buf,

@@ -34,7 +34,7 @@ TOPP_MEMBER_CAP = 8192    # TW_TOPP_MEMBER_CAP
 # every symbol include/twilight.h declares
 EXPORTS = (
     "tw_version", "tw_max_work_items", "tw_quant_append", "tw_quant_build", "tw_quant_rows",
-    "tw_quest_scores", "tw_select", "tw_estimate", "tw_topp", "tw_sparse_attention",
+    "tw_quest_scores", "tw_select", "tw_estimate", "tw_topp", "tw_sparse_attention", "tw_sparse_attention_part",
     "tw_dense_attention", "tw_decode_step", "tw_estimate_tokens", "tw_topp_bisect", "tw_select_estimate_topp",
     "tw_select_estimate_topp_applies", "tw_vec_logits", "tw_vec_softmax", "tw_vec_readout_parts",
     "tw_vec_readout",
@@ -104,6 +104,7 @@ def lib() -> ctypes.CDLL:
         "tw_estimate": ([P, P, P, P, P], ctypes.c_int),
         "tw_topp": ([P, P, P, P], ctypes.c_int),
         "tw_sparse_attention": ([P, P, P, P, P, P], ctypes.c_int),
+        "tw_sparse_attention_part": ([P, P, P, P, P, I32, P], ctypes.c_int),
         "tw_dense_attention": ([P, P, P, P, P], ctypes.c_int),
         "tw_decode_step": ([P, P, P, P, P, P, P, P, P], ctypes.c_int),
         "tw_estimate_tokens": ([P, I32, I32, P, P, I32, P, P, P], ctypes.c_int),

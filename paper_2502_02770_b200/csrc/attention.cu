@@ -578,9 +578,10 @@ int tw_attn_geometry(const tw_paged_kv* kv, int chunk) {
   return TW_OK;
 }
 
+// part: 0 both kernels, 1 the attention kernel only, 2 the merge only (per-kernel timing)
 template <typename T, int G, bool DENSE>
 static int launch_attn(const tw_paged_kv* kv, const T* q, const tw_decode_buffers* buf, float* out, int chunk,
-                       cudaStream_t s) {
+                       cudaStream_t s, int part = 0) {
   const int units = kv->num_seqs * kv->num_kv_heads;
   const int T_tokens = kv->max_pages * kPage;
   const int max_chunks = (T_tokens + chunk - 1) / chunk;
@@ -597,9 +598,13 @@ static int launch_attn(const tw_paged_kv* kv, const T* q, const tw_decode_buffer
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAttThreads, smem);
   int grid = sms * persist_cap(per_sm);
   if (DENSE && grid * kAttWarps > total) grid = (total + kAttWarps - 1) / kAttWarps;
-  if (DENSE) cudaMemsetAsync(buf->counters + 5, 0, sizeof(uint32_t), s);  // dense runs without tw_select
-  launch_pdl(kern, dim3(grid), dim3(kAttThreads), smem, s, *kv, q, *buf, out, chunk, max_chunks, total);
-  launch_pdl(merge_kernel<G, DENSE>, dim3(units * G), dim3(kMergeThreads), 0, s, *kv, *buf, out, chunk, max_chunks);
+  if (part != 2) {
+    if (DENSE) cudaMemsetAsync(buf->counters + 5, 0, sizeof(uint32_t), s);  // dense runs without tw_select
+    else if (part == 1) cudaMemsetAsync(buf->counters + 4, 0, sizeof(uint32_t), s);  // re-runnable alone
+    launch_pdl(kern, dim3(grid), dim3(kAttThreads), smem, s, *kv, q, *buf, out, chunk, max_chunks, total);
+  }
+  if (part != 1)
+    launch_pdl(merge_kernel<G, DENSE>, dim3(units * G), dim3(kMergeThreads), 0, s, *kv, *buf, out, chunk, max_chunks);
   return launch_status();
 }
 
@@ -616,16 +621,23 @@ static inline int sparse_chunk(const tw_decode_params* prm) {
   return prm->chunk_tokens > 0 ? prm->chunk_tokens : kDefaultChunk;
 }
 
-extern "C" int tw_sparse_attention(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
-                                   const tw_decode_buffers* buf, float* out, cudaStream_t stream) {
+extern "C" int tw_sparse_attention_part(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
+                                        const tw_decode_buffers* buf, float* out, int32_t part,
+                                        cudaStream_t stream) {
   if (!kv || !q || !prm || !buf || !out || kv->head_dim != kHeadDim || !buf->partials) return TW_ERR_INVALID;
-  if (prm->renormalize != 1) return TW_ERR_INVALID;
+  if (prm->renormalize != 1 || part < 0 || part > 2) return TW_ERR_INVALID;
   const int chunk = sparse_chunk(prm);
   if (kv->dtype == TW_BF16) {
-    TW_DISPATCH_G(kv->group_size,
-                  (launch_attn<__nv_bfloat16, GG, false>(kv, (const __nv_bfloat16*)q, buf, out, chunk, stream)))
+    TW_DISPATCH_G(kv->group_size, (launch_attn<__nv_bfloat16, GG, false>(kv, (const __nv_bfloat16*)q, buf, out,
+                                                                        chunk, stream, part)))
   }
-  TW_DISPATCH_G(kv->group_size, (launch_attn<float, GG, false>(kv, (const float*)q, buf, out, chunk, stream)))
+  TW_DISPATCH_G(kv->group_size,
+                (launch_attn<float, GG, false>(kv, (const float*)q, buf, out, chunk, stream, part)))
+}
+
+extern "C" int tw_sparse_attention(const tw_paged_kv* kv, const void* q, const tw_decode_params* prm,
+                                   const tw_decode_buffers* buf, float* out, cudaStream_t stream) {
+  return tw_sparse_attention_part(kv, q, prm, buf, out, 0, stream);
 }
 
 // Dense work-item size: 512 tokens once units x chunks give every worker warp

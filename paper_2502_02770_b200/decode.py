@@ -383,6 +383,14 @@ class TwilightDecoder:
                 "tw_sparse_attention")
         return out
 
+    def attend_part(self, q: torch.Tensor, out: torch.Tensor, part: int) -> torch.Tensor:
+        """K4's kernels one at a time (per-kernel timing): 1 the gather / subset
+        softmax kernel, 2 the split-KV merge."""
+        kv, prm, buf = self._args()
+        L.check(L.lib().tw_sparse_attention_part(kv, L.ptr(q), prm, buf, L.ptr(out), int(part),
+                                                 L.stream_handle()), "tw_sparse_attention_part")
+        return out
+
     def dense(self, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if out is None:
             out = self._out()

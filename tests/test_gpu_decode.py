@@ -585,3 +585,23 @@ def test_chunk_geometry_validated_before_any_kernel():
         dec.step(torch.zeros(1, 1, 128, dtype=torch.bfloat16, device="cuda"), k, k)
     torch.cuda.synchronize()
     assert big.seq_lens.tolist() == [0]
+
+
+def test_attention_in_parts_equals_whole():
+    """tw_sparse_attention_part (the bench's per-kernel timing of K4): the
+    attention kernel alone, then the merge alone, reproduce tw_sparse_attention
+    bit for bit, and the attention kernel can be re-run on the same state."""
+    B, H, G, n = 6, 8, 4, 3000
+    dtype = torch.bfloat16
+    cache, batch = _cache(B, H, G, n, dtype, [n, 2900, 1500, 3000, 700, 2048], seed=31, tau=0.7)
+    q = batch.q.contiguous()
+    dec = TwilightDecoder(cache, "quest", budget=1024, p=0.95)
+    whole = dec.forward(q).clone()
+    out = torch.full_like(whole, float("nan"))
+    for _ in range(2):  # re-runnable: the kernel resets its own item counter
+        dec.attend_part(q, out, 1)
+    dec.attend_part(q, out, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(out, whole)
+    with pytest.raises(ValueError):
+        dec.attend_part(q, out, 3)

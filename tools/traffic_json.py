@@ -16,6 +16,7 @@ STAGES = {
     "K3a_estimate": ["estimate_kernel"],
     "K3bc_topp": ["topp_unit", "topp_head"],
     "K4_attention": ["attn_kernel", "merge_kernel"],
+    "K4a_attn_kernel": ["attn_kernel"],
     "K23_unit": ["unit_step"],
 }
 
