@@ -102,3 +102,12 @@ def test_pack_codes_known_answers():
         tw.pack_codes(np.array([7, 3, 12]))
     with pytest.raises(ValueError):
         tw.pack_codes(np.array([16, 0]))
+
+
+def test_bench_roofline_kernel_choice():
+    """bench.py's roofline kernel: the longest stage, and for K4 the attention
+    kernel timed alone (the split-KV merge excluded) when it was measured."""
+    import bench
+    assert bench.dominant_kernel({"K2_select": 5, "K4_attention": 10, "K4a_attn_kernel": 9}) == "K4a_attn_kernel"
+    assert bench.dominant_kernel({"K2_select": 20, "K4_attention": 10, "K4a_attn_kernel": 9}) == "K2_select"
+    assert bench.dominant_kernel({"K2_select": 5, "K4_attention": 10}) == "K4_attention"
