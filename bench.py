@@ -190,13 +190,19 @@ def algorithmic_bytes(cfg, dec, n, elem=2):
     F = sum(b.final_count.sum().item() for b in bl)  # surviving tokens over all units
     k1 = units * (2 * 2 * d * elem + d // 2 + 8 + 2 * 2 * d * elem)          # read k,v; write k,v,codes,params; meta RMW
     k2 = units * (P * 2 * d * elem + G * d * elem + 4 * P) if cfg["selector"] == "quest" else 0
-    k3a = U * 1152                                                            # INT4 codes + fp32 scale/zero per page
-    k3bc = 4 * F                                                              # final index list
+    # K3 is unfused (estimate, then top-p): SURVEY 8(d) adds G*|U|*4*2 -- the
+    # candidates' fp32 logits written by the estimate and read back by top-p
+    # (|U| = U*16 candidate token slots; at C4/C5 ncu sees them reach DRAM)
+    logits = G * U * 16 * 4
+    k3a = U * 1152 + logits                                                   # INT4 codes + fp32 scale/zero per page, logits out
+    k3bc = 4 * F + logits                                                     # logits in, final index list
     k4 = F * (2 * d * elem + 4) + units * G * d * (elem + 4)                  # gathered K,V rows + q + out
     dense = units * n * 2 * d * elem + units * G * d * (elem + 4)
+    k23 = k2 + U * 1152 + 4 * F  # the fused per-unit kernel keeps the logits in L2 / on chip
+    step = k1 + (k23 if getattr(dec, "unit_path", False) else k2 + k3a + k3bc) + k4
     return {"K1_append": k1, "K2_select": k2, "K3a_estimate": k3a, "K3bc_topp": k3bc, "K4_attention": k4,
-            "K4a_attn_kernel": k4,
-            "K23_unit": k2 + k3a + k3bc, "step": k1 + k2 + k3a + k3bc + k4, "K5_dense": dense, "cand_pages": U, "final_tokens": F}
+            "K4a_attn_kernel": k4, "K23_unit": k23, "step": step, "K5_dense": dense, "cand_pages": U,
+            "final_tokens": F, "logits_round_trip": 2 * logits}
 
 
 STAGE_NAMES = ["K1_append", "K2_select", "K3a_estimate", "K3bc_topp", "K4_attention"]
@@ -629,7 +635,13 @@ def run_ours(args, cfg):
                         and kernel_gbs[dominant] / peak < 0.2 else {})},
         "rank_ms": {"min": round(ms_min, 5), "max": round(ms, 5)},
         "step_roofline": {"algorithmic_bytes": ab["step"], "achieved_gbs_per_gpu": round(achieved_step, 1),
-                          "frac": round(achieved_step / peak, 4)},
+                          "frac": round(achieved_step / peak, 4),
+                          **({"logits_round_trip_bytes": ab["logits_round_trip"],
+                              "frac_without_logits": round((ab["step"] - ab["logits_round_trip"]) / (ms * 1e-3) / 1e9
+                                                           / peak, 4),
+                              "note": "K3 is unfused: SURVEY 8(d)'s + G*|U|*4*2 (candidate logits written by the "
+                                      "estimate, read back by top-p) is in the step's bytes"}
+                             if not decs[0].unit_path else {})},
         "kernels_us": {k: round(v * 1e3, 2) for k, v in stage_ms.items()},
         "kernels_gbs": {k: (round(v, 1) if v else None) for k, v in kernel_gbs.items()},
         "algorithmic_bytes": {k: ab[k] for k in stage_ms},
